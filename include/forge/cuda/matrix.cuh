@@ -1,0 +1,372 @@
+// forge/cuda/matrix.cuh — semiring matrix-vector kernels for sm_100a.
+//
+// Reference: prim::matvec / prim::vecmat and detail_mat::{tall,wide}_kernel,
+// run_mat, plan_mat (primitives.hpp:204-244, 611-807).  A is n x p column-major
+// (element (i,j) at j*n + i).
+//
+//   matvec (BLAS gemv 'T', "gevm")   y[j] = op_i f(x[i], A[i,j])
+//     The fold runs down a CONTIGUOUS column.  One warp per (column, row-split);
+//     lanes read 256-bit vectors of the column (ld.global.nc.L1::no_allocate)
+//     and of x (cached: x is re-read by every column and stays in L1/L2).
+//     Commutative ops: lanes stride the column (coalesced) and reduce with a
+//     butterfly.  Non-commutative ops: lane L owns a contiguous run of rows and
+//     the warp reduces in lane order (the reference's tall path keeps row order
+//     the same way, primitives.hpp:606-610).  Tall-skinny shapes split the rows
+//     across warps; the last split to finish (ticket per column) folds the
+//     split partials in split order.
+//
+//   vecmat (BLAS gemv 'N', "gemv")   z[i] = op_j f(A[i,j], x[j])
+//     The fold runs ACROSS columns, so the reference's per-output row view is
+//     strided (primitives.hpp:793-807).  Here every thread owns VE consecutive
+//     rows and walks its columns in order: each step is one 256-bit coalesced
+//     load of A[i..i+VE, j] plus a warp-uniform x[j].  Columns are split across
+//     blocks; the last block of a row-block (ticket) folds the split partials in
+//     split order.  Column order is preserved everywhere, so any associative op
+//     is valid.
+//
+// No tensor cores: both are HBM-bound streaming kernels (<= 0.5 flop/byte).
+#pragma once
+
+#include "forge/cuda/reduce.cuh"
+
+namespace forge::cuda {
+
+constexpr int kMatThreads = 256;
+constexpr int kMatWarps = kMatThreads / kWarp;
+
+template <class T, class S, class F2, class Op>
+struct GevmArgs {
+  const T* A;
+  const T* x;  // nullable when !UsesX
+  S* y;
+  uint64_t n, p;
+  F2 f;        // f(x_elem, a_elem)
+  Op op;
+  uint32_t ks;              // row splits per column
+  uint64_t rows_per_split;  // multiple of 32 * VE
+  bool vec;                 // 256-bit path allowed (alignment)
+  S* partials;              // [p][ks]
+  uint32_t* tickets;        // [p]
+};
+
+template <class T, class S, class F2, class Op, bool UsesX, bool Ordered>
+__global__ void __launch_bounds__(kMatThreads) gevm_kernel(const GevmArgs<T, S, F2, Op> a) {
+  constexpr int VE = mr_vec_elems<T>();
+  constexpr int U = 4;
+  __shared__ bool s_last[kMatWarps];
+  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
+  const uint64_t item = uint64_t(blockIdx.x) * kMatWarps + warp;
+  if (item >= a.p * a.ks) return;
+  const uint64_t j = item / a.ks;
+  const uint32_t s = uint32_t(item % a.ks);
+  const uint64_t r0 = uint64_t(s) * a.rows_per_split;
+  const uint64_t r1 = r0 + a.rows_per_split < a.n ? r0 + a.rows_per_split : a.n;
+  const T* col = a.A + j * a.n;
+  const T xz{};
+  auto fx = [&](const T& xv, const T& av) { return a.f(UsesX ? xv : xz, av); };
+
+  Opt<S> acc{S{}, false};
+  if constexpr (!Ordered) {
+    if (a.vec && VE > 1) {
+      const uint64_t nv = (r1 - r0) / VE;  // r0 is a multiple of 32*VE
+      const T* cv = col + r0;
+      const T* xv = a.x ? a.x + r0 : nullptr;
+      uint64_t k = lane;
+      S vacc[VE];
+      bool vh = false;
+      for (; k + uint64_t(kWarp) * (U - 1) < nv; k += uint64_t(kWarp) * U) {
+        T av[U][VE], xx[U][VE];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          load_items<T, VE>(cv + (k + u * kWarp) * VE, av[u]);
+          if constexpr (UsesX) load_items<T, VE, false>(xv + (k + u * kWarp) * VE, xx[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < VE; ++e) {
+            S t = fx(UsesX ? xx[u][e] : xz, av[u][e]);
+            vacc[e] = (vh || u > 0) ? a.op(vacc[e], t) : t;
+          }
+        vh = true;
+      }
+      for (; k < nv; k += kWarp) {
+        T av[VE], xx[VE];
+        load_items<T, VE>(cv + k * VE, av);
+        if constexpr (UsesX) load_items<T, VE, false>(xv + k * VE, xx);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          S t = fx(UsesX ? xx[e] : xz, av[e]);
+          vacc[e] = vh ? a.op(vacc[e], t) : t;
+        }
+        vh = true;
+      }
+      if (vh) {
+        S t = vacc[0];
+#pragma unroll
+        for (int e = 1; e < VE; ++e) t = a.op(t, vacc[e]);
+        acc = Opt<S>{t, true};
+      }
+      for (uint64_t i = r0 + nv * VE + lane; i < r1; i += kWarp)
+        acc = opt_combine(a.op, acc, Opt<S>{fx(UsesX ? a.x[i] : xz, col[i]), true});
+    } else {
+      for (uint64_t i = r0 + lane; i < r1; i += kWarp)
+        acc = opt_combine(a.op, acc, Opt<S>{fx(UsesX ? a.x[i] : xz, col[i]), true});
+    }
+    acc = warp_allreduce_comm(a.op, acc);
+  } else {
+    // Lane-contiguous runs of rows, folded in row order, then an ordered warp tree.
+    const uint64_t len = r1 - r0;
+    uint64_t per = ceil_div(len, kWarp);
+    if (VE > 1) per = round_up(per, VE);
+    const uint64_t lo = r0 + lane * per < r1 ? r0 + lane * per : r1;
+    const uint64_t hi = lo + per < r1 ? lo + per : r1;
+    uint64_t i = lo;
+    if (a.vec && VE > 1) {
+      for (; i + VE <= hi; i += VE) {
+        T av[VE], xx[VE];
+        load_items<T, VE>(col + i, av);
+        if constexpr (UsesX) load_items<T, VE, false>(a.x + i, xx);
+#pragma unroll
+        for (int e = 0; e < VE; ++e)
+          acc = opt_combine(a.op, acc, Opt<S>{fx(UsesX ? xx[e] : xz, av[e]), true});
+      }
+    }
+    for (; i < hi; ++i) acc = opt_combine(a.op, acc, Opt<S>{fx(UsesX ? a.x[i] : xz, col[i]), true});
+    acc = warp_reduce_ordered(a.op, acc);
+  }
+
+  if (a.ks == 1) {
+    if (lane == 0) a.y[j] = acc.v;
+    return;
+  }
+  // Split partial; the last split to arrive folds all splits in order.
+  if (lane == 0) {
+    a.partials[j * a.ks + s] = acc.v;
+    const uint32_t t = atom_add_acq_rel_gpu(a.tickets + j, 1u);
+    s_last[warp] = (t == a.ks - 1);
+    if (s_last[warp]) st_relaxed_gpu(a.tickets + j, 0u);
+  }
+  __syncwarp();
+  if (!s_last[warp]) return;
+  if (lane == 0) {
+    S v = ld_strong(a.partials + j * a.ks);
+    for (uint32_t q = 1; q < a.ks; ++q) v = a.op(v, ld_strong(a.partials + j * a.ks + q));
+    a.y[j] = v;
+  }
+}
+
+template <class T, class S, class F2, class Op>
+struct GemvArgs {
+  const T* A;
+  const T* x;
+  S* z;
+  uint64_t n, p;
+  F2 f;  // f(a_elem, x_elem)
+  Op op;
+  uint32_t ks;              // column splits
+  uint64_t cols_per_split;
+  uint32_t row_blocks;
+  bool vec;
+  S* partials;        // [ks][n]
+  uint32_t* tickets;  // [row_blocks]
+};
+
+template <class T>
+constexpr int gemv_vec_elems() {
+  return mr_vec_elems<T>();
+}
+
+template <class T, class S, class F2, class Op, bool UsesX>
+__global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, F2, Op> a) {
+  constexpr int VE = gemv_vec_elems<T>();
+  constexpr int U = 4;
+  __shared__ bool s_last;
+  const uint32_t rb = blockIdx.x % a.row_blocks;
+  const uint32_t s = blockIdx.x / a.row_blocks;
+  const uint64_t c0 = uint64_t(s) * a.cols_per_split;
+  const uint64_t c1 = c0 + a.cols_per_split < a.p ? c0 + a.cols_per_split : a.p;
+  const uint64_t i0 = (uint64_t(rb) * kMatThreads + threadIdx.x) * VE;  // first row of this thread
+  const T xz{};
+  auto fa = [&](const T& av, const T& xv) { return a.f(av, UsesX ? xv : xz); };
+
+  S acc[VE];
+  const bool full = i0 + VE <= a.n;
+  if (i0 < a.n && c0 < c1) {
+    if (full && a.vec) {
+      uint64_t j = c0;
+      {
+        T av[VE];
+        load_items<T, VE>(a.A + j * a.n + i0, av);
+        const T xj = UsesX ? a.x[j] : xz;
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc[e] = fa(av[e], xj);
+        ++j;
+      }
+      for (; j + U <= c1; j += U) {
+        T av[U][VE];
+        T xj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          load_items<T, VE>(a.A + (j + u) * a.n + i0, av[u]);
+          xj[u] = UsesX ? a.x[j + u] : xz;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < VE; ++e) acc[e] = a.op(acc[e], fa(av[u][e], xj[u]));
+      }
+      for (; j < c1; ++j) {
+        T av[VE];
+        load_items<T, VE>(a.A + j * a.n + i0, av);
+        const T xj = UsesX ? a.x[j] : xz;
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc[e] = a.op(acc[e], fa(av[e], xj));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        const uint64_t i = i0 + e;
+        if (i < a.n) {
+          S v = fa(a.A[c0 * a.n + i], UsesX ? a.x[c0] : xz);
+          for (uint64_t j = c0 + 1; j < c1; ++j) v = a.op(v, fa(a.A[j * a.n + i], UsesX ? a.x[j] : xz));
+          acc[e] = v;
+        }
+      }
+    }
+  }
+
+  if (a.ks == 1) {
+    if (i0 < a.n) {
+      if (full && a.vec) {
+        store_items<S, VE>(a.z + i0, acc);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e)
+          if (i0 + e < a.n) a.z[i0 + e] = acc[e];
+      }
+    }
+    return;
+  }
+  // Partials [s][row]; last block of this row-block folds in split order.
+  if (i0 < a.n) {
+#pragma unroll
+    for (int e = 0; e < VE; ++e)
+      if (i0 + e < a.n) a.partials[uint64_t(s) * a.n + i0 + e] = acc[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t t = atom_add_acq_rel_gpu(a.tickets + rb, 1u);
+    s_last = (t == a.ks - 1);
+    if (s_last) st_relaxed_gpu(a.tickets + rb, 0u);
+  }
+  __syncthreads();
+  if (!s_last) return;
+#pragma unroll
+  for (int e = 0; e < VE; ++e) {
+    const uint64_t i = i0 + e;
+    if (i < a.n) {
+      S v = ld_strong(a.partials + i);
+      for (uint32_t q = 1; q < a.ks; ++q) v = a.op(v, ld_strong(a.partials + uint64_t(q) * a.n + i));
+      a.z[i] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Planning + workspace (the B200 counterpart of plan_mat, primitives.hpp:220-244).
+
+struct GevmPlan {
+  uint32_t ks;
+  uint64_t rows_per_split;
+  uint64_t grid;
+};
+
+template <class T>
+inline GevmPlan plan_gevm(uint64_t n, uint64_t p) {
+  constexpr int VE = mr_vec_elems<T>();
+  const uint64_t target_warps = uint64_t(device_props().sm_count) * 48;
+  const uint64_t gran = uint64_t(kWarp) * VE * 4;  // rows per warp step
+  uint64_t ks = p >= target_warps ? 1 : ceil_div(target_warps, p);
+  const uint64_t max_ks = ceil_div(n, gran * 4);  // keep >= 4 steps per split
+  if (ks > max_ks) ks = max_ks;
+  if (ks < 1) ks = 1;
+  if (ks > 4096) ks = 4096;
+  uint64_t rps = round_up(ceil_div(n, ks), uint64_t(kWarp) * VE);
+  ks = ceil_div(n, rps);
+  if (ks < 1) ks = 1;
+  GevmPlan pl{uint32_t(ks), rps, ceil_div(p * ks, kMatWarps)};
+  return pl;
+}
+
+struct GemvPlan {
+  uint32_t ks;
+  uint64_t cols_per_split;
+  uint32_t row_blocks;
+  uint64_t grid;
+};
+
+template <class T>
+inline GemvPlan plan_gemv(uint64_t n, uint64_t p) {
+  constexpr int VE = gemv_vec_elems<T>();
+  const uint64_t row_blocks = ceil_div(n, uint64_t(kMatThreads) * VE);
+  const uint64_t target_blocks = uint64_t(device_props().sm_count) * 4;
+  uint64_t ks = row_blocks >= target_blocks ? 1 : ceil_div(target_blocks, row_blocks);
+  const uint64_t max_ks = ceil_div(p, 16);  // >= 16 columns per split
+  if (ks > max_ks) ks = max_ks;
+  if (ks < 1) ks = 1;
+  uint64_t cps = ceil_div(p, ks);
+  ks = ceil_div(p, cps);
+  if (ks < 1) ks = 1;
+  return GemvPlan{uint32_t(ks), cps, uint32_t(row_blocks), row_blocks * ks};
+}
+
+template <class T, class S>
+inline uint64_t gevm_ws_bytes(uint64_t n, uint64_t p) {
+  GevmPlan pl = plan_gevm<T>(n, p);
+  if (pl.ks == 1) return 256;
+  return 256 + round_up(p * sizeof(uint32_t), 256) + p * pl.ks * sizeof(S);
+}
+
+template <class T, class S>
+inline uint64_t gemv_ws_bytes(uint64_t n, uint64_t p) {
+  GemvPlan pl = plan_gemv<T>(n, p);
+  if (pl.ks == 1) return 256;
+  return 256 + round_up(uint64_t(pl.row_blocks) * sizeof(uint32_t), 256) + uint64_t(pl.ks) * n * sizeof(S);
+}
+
+template <class T, class S, class F2, class Op, bool UsesX, bool Ordered>
+cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, const F2& f,
+                        const Op& op, void* ws, cudaStream_t stream) {
+  if (p == 0 || n == 0) return cudaSuccess;
+  constexpr int VE = mr_vec_elems<T>();
+  GevmPlan pl = plan_gevm<T>(n, p);
+  GevmArgs<T, S, F2, Op> a{A, x, y, n, p, f, op, pl.ks, pl.rows_per_split, false, nullptr, nullptr};
+  a.vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && (!UsesX || is_aligned(x, 32));
+  if (pl.ks > 1) {
+    char* w = static_cast<char*>(ws) + 256;
+    a.tickets = reinterpret_cast<uint32_t*>(w);
+    a.partials = reinterpret_cast<S*>(w + round_up(p * sizeof(uint32_t), 256));
+  }
+  gevm_kernel<T, S, F2, Op, UsesX, Ordered><<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <class T, class S, class F2, class Op, bool UsesX>
+cudaError_t launch_gemv(const T* A, uint64_t n, uint64_t p, const T* x, S* z, const F2& f,
+                        const Op& op, void* ws, cudaStream_t stream) {
+  if (p == 0 || n == 0) return cudaSuccess;
+  constexpr int VE = gemv_vec_elems<T>();
+  GemvPlan pl = plan_gemv<T>(n, p);
+  GemvArgs<T, S, F2, Op> a{A, x, z, n, p, f, op, pl.ks, pl.cols_per_split, pl.row_blocks, false, nullptr, nullptr};
+  a.vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && is_aligned(z, 32);
+  if (pl.ks > 1) {
+    char* w = static_cast<char*>(ws) + 256;
+    a.tickets = reinterpret_cast<uint32_t*>(w);
+    a.partials = reinterpret_cast<S*>(w + round_up(uint64_t(pl.row_blocks) * sizeof(uint32_t), 256));
+  }
+  gemv_kernel<T, S, F2, Op, UsesX><<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace forge::cuda

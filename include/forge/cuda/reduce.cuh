@@ -1,0 +1,418 @@
+// forge/cuda/reduce.cuh — one-kernel mapreduce, the order-preserving reduce and
+// the rank-order fold.
+//
+// Reference: prim::mapreduce (primitives.hpp:348-431).  The reference runs a
+// fixed grid of 100 x 256 threads, a grid-stride scalar map, an ordered warp
+// tree, a shared-memory cross-warp step, and block 0 spinning on the release
+// flags of every other block (a forward-progress hazard on real hardware:
+// block 0 may spin while blocks it waits for are not yet resident).
+//
+// sm_100a design:
+//   * grid = #SM x resident CTAs (persistent style), 256 threads;
+//   * 256-bit ld.global.nc.L1::no_allocate.v8 loads, UNROLL independent vectors
+//     in flight per thread (128 B/thread, tens of MB chip-wide), NACC
+//     independent per-thread accumulators (ILP and a shallower float chain);
+//   * warp butterfly (mapreduce requires a commutative op) + smem cross-warp;
+//   * inter-block: every block stores its partial and does ONE acq_rel ticket
+//     RMW; the LAST block to arrive (not block 0) folds the partials in block
+//     order.  No block ever waits for another, so there is no residency
+//     assumption, the result is deterministic for a fixed grid, and the ticket
+//     self-resets so the workspace needs no memset between launches.
+#pragma once
+
+#include "forge/cuda/device.cuh"
+
+namespace forge::cuda {
+
+constexpr int kReduceThreads = 256;
+
+// Carry type for the sequential cross-tile chains (decoupled look-back carry,
+// per-block tile accumulation of the ordered reduce).  Default: S itself.  An
+// op opts into a wider carry by defining `using carry_traits = ...;` with the
+// same static members (the menu's f32 sums carry in f64, the affine maps in
+// Affine<double>); per-element work always stays in S.
+template <class S, class Op, class = void>
+struct CarryTraits {
+  using C = S;
+  static __device__ __forceinline__ C to_c(const S& s) { return s; }
+  static __device__ __forceinline__ S to_s(const C& c) { return c; }
+  static __device__ __forceinline__ C op(const Op& o, const C& a, const C& b) { return o(a, b); }
+};
+
+template <class S, class Op>
+struct CarryTraits<S, Op, std::void_t<typename Op::carry_traits>> : Op::carry_traits {};
+
+template <class T>
+constexpr int mr_vec_elems() {
+  return (sizeof(T) <= 32 && (32 % sizeof(T)) == 0) ? int(32 / sizeof(T)) : 1;
+}
+
+// Block-wide commutative reduction; the result is valid in thread 0.
+template <class S, class Op>
+__device__ __forceinline__ Opt<S> block_reduce_comm(const Op& op, Opt<S> v, Opt<S>* smem) {
+  v = warp_allreduce_comm(op, v);
+  const unsigned warp = threadIdx.x / kWarp, lane = lane_id();
+  const unsigned nwarps = blockDim.x / kWarp;
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    Opt<S> w = lane < nwarps ? smem[lane] : Opt<S>{S{}, false};
+    w = warp_allreduce_comm(op, w);
+    if (lane == 0) v = w;
+  }
+  __syncthreads();
+  return v;
+}
+
+// Block-wide ORDERED reduction of one value per thread in thread order; the
+// result is valid in thread 0.
+template <class S, class Op>
+__device__ __forceinline__ Opt<S> block_reduce_ordered(const Op& op, Opt<S> v, Opt<S>* smem) {
+  v = warp_reduce_ordered(op, v);
+  const unsigned warp = threadIdx.x / kWarp, lane = lane_id();
+  const unsigned nwarps = blockDim.x / kWarp;
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    Opt<S> w = lane < nwarps ? smem[lane] : Opt<S>{S{}, false};
+    w = warp_reduce_ordered(op, w);
+    if (lane == 0) v = w;
+  }
+  __syncthreads();
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// mapreduce (commutative)
+
+template <class T, class S, class F, class Op>
+struct MapReduceArgs {
+  const T* src;
+  uint64_t n;
+  uint64_t stride;  // in elements; 1 = contiguous
+  F f;
+  Op op;
+  S* partials;         // [grid]
+  uint32_t* part_has;  // [grid]
+  uint32_t* ticket;    // self-resetting arrival counter
+  S* out;              // device result (S)
+  uint32_t* out_has;   // nullable
+};
+
+template <class T, class S, class F, class Op, int UNROLL>
+__global__ void __launch_bounds__(kReduceThreads)
+    mapreduce_kernel(const MapReduceArgs<T, S, F, Op> a) {
+  constexpr int VE = mr_vec_elems<T>();
+  constexpr int VB = VE * int(sizeof(T));
+  constexpr int NACC = VE < 8 ? VE : 8;
+  constexpr uint64_t kChunk = uint64_t(kReduceThreads) * UNROLL;
+  __shared__ Opt<S> smem[kReduceThreads / kWarp];
+  __shared__ bool s_last;
+
+  const uint64_t gtid = uint64_t(blockIdx.x) * kReduceThreads + threadIdx.x;
+  const uint64_t gsize = uint64_t(gridDim.x) * kReduceThreads;
+
+  S acc[NACC];       // vector accumulators, valid iff vhas
+  bool vhas = false;
+  Opt<S> sacc{S{}, false};  // scalar (head / tail / strided) accumulator
+
+  const bool vector_path =
+      VE > 1 && a.stride == 1 && (reinterpret_cast<uintptr_t>(a.src) % sizeof(T)) == 0;
+  if (vector_path) {
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(a.src);
+    uint64_t head = ((VB - (addr % VB)) % VB) / sizeof(T);
+    if (head > a.n) head = a.n;
+    const uint64_t nvec = (a.n - head) / VE;
+    const T* body = a.src + head;
+    const uint64_t full_chunks = nvec / kChunk;
+    uint64_t c = blockIdx.x;
+    if (c < full_chunks) {
+      T x[UNROLL][VE];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        load_items<T, VE>(body + (c * kChunk + u * kReduceThreads + threadIdx.x) * VE, x[u]);
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) acc[k] = a.f(x[0][k]);
+#pragma unroll
+      for (int k = NACC; k < VE; ++k) acc[k % NACC] = a.op(acc[k % NACC], a.f(x[0][k]));
+#pragma unroll
+      for (int u = 1; u < UNROLL; ++u)
+#pragma unroll
+        for (int k = 0; k < VE; ++k) acc[k % NACC] = a.op(acc[k % NACC], a.f(x[u][k]));
+      vhas = true;
+      for (c += gridDim.x; c < full_chunks; c += gridDim.x) {
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          load_items<T, VE>(body + (c * kChunk + u * kReduceThreads + threadIdx.x) * VE, x[u]);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+          for (int k = 0; k < VE; ++k) acc[k % NACC] = a.op(acc[k % NACC], a.f(x[u][k]));
+      }
+    }
+    // Leftover whole vectors, one per thread per pass.
+    for (uint64_t v = full_chunks * kChunk + gtid; v < nvec; v += gsize) {
+      T x[VE];
+      load_items<T, VE>(body + v * VE, x);
+      if (!vhas) {
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) acc[k] = a.f(x[k]);
+#pragma unroll
+        for (int k = NACC; k < VE; ++k) acc[k % NACC] = a.op(acc[k % NACC], a.f(x[k]));
+        vhas = true;
+      } else {
+#pragma unroll
+        for (int k = 0; k < VE; ++k) acc[k % NACC] = a.op(acc[k % NACC], a.f(x[k]));
+      }
+    }
+    // Head and tail elements (fewer than 2*VE) go to the first threads.
+    const uint64_t tail0 = head + nvec * VE;
+    const uint64_t extra = head + (a.n - tail0);
+    for (uint64_t e = gtid; e < extra; e += gsize) {
+      const uint64_t i = e < head ? e : tail0 + (e - head);
+      sacc = opt_combine(a.op, sacc, Opt<S>{a.f(a.src[i]), true});
+    }
+  } else {
+    for (uint64_t i = gtid; i < a.n; i += gsize)
+      sacc = opt_combine(a.op, sacc, Opt<S>{a.f(a.src[i * a.stride]), true});
+  }
+
+  Opt<S> mine = sacc;
+  if (vhas) {
+    S t = acc[0];
+#pragma unroll
+    for (int k = 1; k < NACC; ++k) t = a.op(t, acc[k]);
+    mine = opt_combine(a.op, mine, Opt<S>{t, true});
+  }
+  Opt<S> blk = block_reduce_comm(a.op, mine, smem);
+
+  if (threadIdx.x == 0) {
+    a.partials[blockIdx.x] = blk.v;
+    a.part_has[blockIdx.x] = blk.has ? 1u : 0u;
+    const uint32_t t = atom_add_acq_rel_gpu(a.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) st_relaxed_gpu(a.ticket, 0u);  // every block has arrived: reset for reuse
+  }
+  __syncthreads();
+  if (!s_last) return;
+
+  // Last block: fold the partials (deterministic tree for a fixed grid).
+  Opt<S> v{S{}, false};
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kReduceThreads) {
+    if (ld_relaxed_gpu(a.part_has + b)) v = opt_combine(a.op, v, Opt<S>{ld_strong(a.partials + b), true});
+  }
+  Opt<S> total = block_reduce_comm(a.op, v, smem);
+  if (threadIdx.x == 0) {
+    *a.out = total.v;
+    if (a.out_has) *a.out_has = total.has ? 1u : 0u;
+  }
+}
+
+template <class T>
+constexpr int mr_unroll() {
+  return mr_vec_elems<T>() > 1 ? 4 : 8;
+}
+
+// Workspace layout (bytes) for mapreduce with `grid` blocks.
+template <class S>
+struct MapReduceWs {
+  static constexpr uint64_t align(uint64_t v) { return (v + 255) & ~uint64_t(255); }
+  static uint64_t bytes(uint32_t grid) {
+    return align(sizeof(uint32_t) * 4) + align(uint64_t(grid) * sizeof(S)) +
+           align(uint64_t(grid) * sizeof(uint32_t));
+  }
+  static void carve(void* ws, uint32_t grid, uint32_t*& ticket, S*& partials, uint32_t*& has) {
+    char* p = static_cast<char*>(ws);
+    ticket = reinterpret_cast<uint32_t*>(p);
+    p += align(sizeof(uint32_t) * 4);
+    partials = reinterpret_cast<S*>(p);
+    p += align(uint64_t(grid) * sizeof(S));
+    has = reinterpret_cast<uint32_t*>(p);
+  }
+};
+
+inline uint32_t mapreduce_max_grid() { return uint32_t(device_props().sm_count) * 4; }
+
+template <class T>
+inline uint32_t mapreduce_grid(uint64_t n) {
+  constexpr uint64_t per_block = uint64_t(kReduceThreads) * mr_vec_elems<T>() * mr_unroll<T>();
+  uint64_t want = ceil_div(n, per_block);
+  uint64_t cap = mapreduce_max_grid();
+  return uint32_t(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+// Launch; `ws` holds MapReduceWs<S>::bytes(mapreduce_max_grid()) zero-initialised bytes.
+template <class T, class S, class F, class Op>
+cudaError_t launch_mapreduce(const T* src, uint64_t n, uint64_t stride, const F& f, const Op& op,
+                             S* out_dev, uint32_t* out_has_dev, void* ws, cudaStream_t stream) {
+  const uint32_t grid = mapreduce_grid<T>(stride == 1 ? n : n * 4);
+  MapReduceArgs<T, S, F, Op> a{src, n, stride, f, op, nullptr, nullptr, nullptr, out_dev, out_has_dev};
+  MapReduceWs<S>::carve(ws, mapreduce_max_grid(), a.ticket, a.partials, a.part_has);
+  mapreduce_kernel<T, S, F, Op, mr_unroll<T>()><<<grid, kReduceThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Order-preserving reduce: any associative op.  Block b owns a contiguous run
+// of tiles; inside a tile each thread folds ITEMS contiguous elements in order,
+// then an ordered warp/block tree; tiles are folded in order into a C carry;
+// the last block to arrive folds the block partials in block order.
+
+// Items per thread of a scan tile: 64 bytes of S (16 f32, 8 eight-byte structs,
+// 4 sixteen-byte structs).  Depends on S only so that a workspace sized for S
+// fits every T.
+template <class S>
+constexpr int scan_items() {
+  constexpr int it = 64 / int(sizeof(S));
+  return it < 1 ? 1 : (it > 16 ? 16 : it);
+}
+
+template <class T, class S>
+constexpr int tile_items() {
+  constexpr int big = sizeof(T) > sizeof(S) ? int(sizeof(T)) : int(sizeof(S));
+  constexpr int it = 64 / big;
+  return it < 1 ? 1 : (it > 16 ? 16 : it);
+}
+
+template <class T, class S, class F, class Op, class C>
+struct OrderedReduceArgs {
+  const T* src;
+  uint64_t n;
+  uint64_t stride;
+  F f;
+  Op op;
+  uint64_t tiles_per_block;
+  C* partials;
+  uint32_t* part_has;
+  uint32_t* ticket;
+  S* out;
+  uint32_t* out_has;
+};
+
+template <class T, class S, class F, class Op>
+__global__ void __launch_bounds__(kReduceThreads)
+    reduce_ordered_kernel(const OrderedReduceArgs<T, S, F, Op, typename CarryTraits<S, Op>::C> a) {
+  using CT = CarryTraits<S, Op>;
+  using C = typename CT::C;
+  constexpr int IT = tile_items<T, S>();
+  constexpr uint64_t kTile = uint64_t(kReduceThreads) * IT;
+  __shared__ Opt<S> smem[kReduceThreads / kWarp];
+  __shared__ Opt<C> csmem[kWarp];
+  __shared__ bool s_last;
+  auto cop = [&](const C& x, const C& y) { return CT::op(a.op, x, y); };
+
+  const uint64_t ntiles = ceil_div(a.n, kTile);
+  const uint64_t t0 = uint64_t(blockIdx.x) * a.tiles_per_block;
+  const uint64_t t1 = t0 + a.tiles_per_block < ntiles ? t0 + a.tiles_per_block : ntiles;
+  const bool vec_ok = a.stride == 1 && is_aligned(a.src, items_align<T, IT>());
+  Opt<C> bacc{C{}, false};  // meaningful in thread 0
+  for (uint64_t t = t0; t < t1; ++t) {
+    const uint64_t base = t * kTile + uint64_t(threadIdx.x) * IT;
+    Opt<S> mine{S{}, false};
+    if (base + IT <= a.n && vec_ok) {
+      T x[IT];
+      load_items<T, IT>(a.src + base, x);
+      S v = a.f(x[0]);
+#pragma unroll
+      for (int k = 1; k < IT; ++k) v = a.op(v, a.f(x[k]));
+      mine = Opt<S>{v, true};
+    } else {
+      for (int k = 0; k < IT; ++k) {
+        if (base + k < a.n) mine = opt_combine(a.op, mine, Opt<S>{a.f(a.src[(base + k) * a.stride]), true});
+      }
+    }
+    Opt<S> tile = block_reduce_ordered(a.op, mine, smem);
+    if (threadIdx.x == 0 && tile.has) {
+      C tc = CT::to_c(tile.v);
+      bacc = bacc.has ? Opt<C>{cop(bacc.v, tc), true} : Opt<C>{tc, true};
+    }
+  }
+  if (threadIdx.x == 0) {
+    a.partials[blockIdx.x] = bacc.v;
+    a.part_has[blockIdx.x] = bacc.has ? 1u : 0u;
+    const uint32_t t = atom_add_acq_rel_gpu(a.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) st_relaxed_gpu(a.ticket, 0u);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // Last block: warp 0 folds partials in block order.  Lane L owns a
+  // contiguous range of blocks, then an ordered warp reduction.
+  if (threadIdx.x >= kWarp) return;
+  const uint32_t nb = gridDim.x;
+  const uint32_t per = (nb + kWarp - 1) / kWarp;
+  const uint32_t lo = threadIdx.x * per, hi = lo + per < nb ? lo + per : nb;
+  Opt<C> v{C{}, false};
+  for (uint32_t b = lo; b < hi; ++b) {
+    if (ld_relaxed_gpu(a.part_has + b)) {
+      C pb = ld_strong(a.partials + b);
+      v = v.has ? Opt<C>{cop(v.v, pb), true} : Opt<C>{pb, true};
+    }
+  }
+  v = warp_reduce_ordered(cop, v);
+  if (threadIdx.x == 0) {
+    *a.out = CT::to_s(v.v);
+    if (a.out_has) *a.out_has = v.has ? 1u : 0u;
+  }
+  (void)csmem;
+}
+
+template <class S, class Op>
+struct OrderedReduceWs {
+  using C = typename CarryTraits<S, Op>::C;
+  static constexpr uint64_t align(uint64_t v) { return (v + 255) & ~uint64_t(255); }
+  static uint64_t bytes(uint32_t grid) {
+    return align(sizeof(uint32_t) * 4) + align(uint64_t(grid) * sizeof(C)) +
+           align(uint64_t(grid) * sizeof(uint32_t));
+  }
+  static void carve(void* ws, uint32_t grid, uint32_t*& ticket, C*& partials, uint32_t*& has) {
+    char* p = static_cast<char*>(ws);
+    ticket = reinterpret_cast<uint32_t*>(p);
+    p += align(sizeof(uint32_t) * 4);
+    partials = reinterpret_cast<C*>(p);
+    p += align(uint64_t(grid) * sizeof(C));
+    has = reinterpret_cast<uint32_t*>(p);
+  }
+};
+
+template <class T, class S, class F, class Op>
+cudaError_t launch_reduce_ordered(const T* src, uint64_t n, uint64_t stride, const F& f,
+                                  const Op& op, S* out_dev, uint32_t* out_has_dev, void* ws,
+                                  cudaStream_t stream) {
+  using C = typename CarryTraits<S, Op>::C;
+  constexpr uint64_t kTile = uint64_t(kReduceThreads) * tile_items<T, S>();
+  const uint64_t ntiles = ceil_div(n, kTile);
+  const uint32_t cap = mapreduce_max_grid();
+  uint64_t grid = ntiles < cap ? ntiles : cap;
+  if (grid < 1) grid = 1;
+  const uint64_t per = ceil_div(ntiles, grid);
+  grid = ntiles ? ceil_div(ntiles, per) : 1;
+  OrderedReduceArgs<T, S, F, Op, C> a{src, n, stride, f, op, per, nullptr, nullptr, nullptr, out_dev, out_has_dev};
+  OrderedReduceWs<S, Op>::carve(ws, cap, a.ticket, a.partials, a.part_has);
+  reduce_ordered_kernel<T, S, F, Op><<<uint32_t(grid), kReduceThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Fold of a short device array in index order (rank-order fold of the sharded
+// exchange).  upto < 0: all `count` values; else values[0..upto).
+
+template <class S, class Op>
+__global__ void fold_kernel(const S* values, uint32_t count, int32_t upto, Op op, S* out,
+                            int32_t* has_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint32_t m = upto < 0 ? count : (uint32_t(upto) < count ? uint32_t(upto) : count);
+  Opt<S> v{S{}, false};
+  for (uint32_t i = 0; i < m; ++i) v = opt_combine(op, v, Opt<S>{values[i], true});
+  if (v.has) *out = v.v;
+  if (has_out) *has_out = v.has ? 1 : 0;
+}
+
+template <class S, class Op>
+cudaError_t launch_fold(const S* values, uint32_t count, int32_t upto, const Op& op, S* out,
+                        int32_t* has_out, cudaStream_t stream) {
+  fold_kernel<S, Op><<<1, 32, 0, stream>>>(values, count, upto, op, out, has_out);
+  return cudaGetLastError();
+}
+
+}  // namespace forge::cuda

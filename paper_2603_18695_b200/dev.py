@@ -1,0 +1,108 @@
+"""Device-pointer layer over the C-ABI for torch-tensor callers.
+
+torch provides HBM allocations and streams (plumbing); every computation is a
+libforge.so sm_100a kernel launched on the given stream.  Tensors are passed by
+data_ptr(); element types are the op's T / S (struct types travel as uint8
+tensors of n * sizeof bytes).  All calls are asynchronous and stream-ordered.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import capi
+from .forge import ForgeError, check, op_info
+
+
+def _lib():
+    return capi.load()
+
+
+def _stream(stream) -> C.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _ptr(t) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(0)
+    if isinstance(t, int):
+        return C.c_void_p(t)
+    if not t.is_cuda:
+        raise ForgeError(capi.ERR_INVALID_ARGUMENT, "tensor must live on a CUDA device")
+    return C.c_void_p(t.data_ptr())
+
+
+def workspace_bytes(prim: int, op: int, n: int, p_cols: int = 0) -> int:
+    out = C.c_uint64()
+    check(_lib().forge_dev_workspace_bytes(prim, op, n, p_cols, C.byref(out)))
+    return out.value
+
+
+class Workspace:
+    """A zero-initialised device byte buffer, grown on demand.  The kernels
+    leave it reusable (self-resetting tickets / epochs); it must not be used by
+    two launches in flight at once."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.buf = torch.zeros(256, dtype=torch.uint8, device=self.device)
+
+    def ensure(self, nbytes: int) -> torch.Tensor:
+        if self.buf.numel() < nbytes:
+            self.buf = torch.zeros(max(nbytes, 2 * self.buf.numel()), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+    def for_(self, prim: int, op: int, n: int, p_cols: int = 0) -> tuple[C.c_void_p, int]:
+        need = workspace_bytes(prim, op, n, p_cols)
+        b = self.ensure(need)
+        return C.c_void_p(b.data_ptr()), b.numel()
+
+
+def empty(op: int, n: int, which: str = "T", device=None) -> torch.Tensor:
+    info = op_info(op)
+    size = info["t_size"] if which == "T" else info["s_size"]
+    return torch.empty(n * size, dtype=torch.uint8, device=device or "cuda")
+
+
+def fill_synthetic(op: int, dst: torch.Tensor, n: int, seed: int, index_base: int = 0, variant: int = 0,
+                   stream=None) -> None:
+    check(_lib().forge_dev_fill_synthetic(op, _ptr(dst), n, seed, index_base, variant, _stream(stream)))
+
+
+def mapreduce(op: int, src, n: int, out, ws: Workspace, stream=None) -> None:
+    w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n)
+    check(_lib().forge_dev_mapreduce(op, _ptr(src), n, _ptr(out), w, wb, _stream(stream)))
+
+
+def reduce_ordered(op: int, src, n: int, out, ws: Workspace, stream=None) -> None:
+    w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n)
+    check(_lib().forge_dev_reduce_ordered(op, _ptr(src), n, _ptr(out), w, wb, _stream(stream)))
+
+
+def scan(op: int, inclusive: bool, src, dst, n: int, ws: Workspace, carry_in=None, total_out=None,
+         stream=None) -> None:
+    w, wb = ws.for_(capi.PRIM_SCAN, op, n)
+    check(_lib().forge_dev_scan(op, 1 if inclusive else 0, _ptr(src), _ptr(dst), n, _ptr(carry_in),
+                                _ptr(total_out), w, wb, _stream(stream)))
+
+
+def matvec(op: int, A, n: int, p_cols: int, x, y, ws: Workspace, stream=None) -> None:
+    w, wb = ws.for_(capi.PRIM_MATVEC, op, n, p_cols)
+    check(_lib().forge_dev_matvec(op, _ptr(A), n, p_cols, _ptr(x), _ptr(y), w, wb, _stream(stream)))
+
+
+def vecmat(op: int, A, n: int, p_cols: int, x, z, ws: Workspace, stream=None) -> None:
+    w, wb = ws.for_(capi.PRIM_VECMAT, op, n, p_cols)
+    check(_lib().forge_dev_vecmat(op, _ptr(A), n, p_cols, _ptr(x), _ptr(z), w, wb, _stream(stream)))
+
+
+def fold(op: int, values, count: int, out, exclusive_upto: int = -1, has_out=None, stream=None) -> None:
+    check(_lib().forge_dev_fold(op, _ptr(values), count, exclusive_upto, _ptr(out), _ptr(has_out),
+                                _stream(stream)))
+
+
+def copy(src, dst, nbytes: int, stream=None) -> None:
+    check(_lib().forge_dev_copy(_ptr(src), _ptr(dst), nbytes, _stream(stream)))
