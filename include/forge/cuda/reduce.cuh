@@ -31,9 +31,17 @@ constexpr int kReduceThreads = 256;
 // op opts into a wider carry by defining `using carry_traits = ...;` with the
 // same static members (the menu's f32 sums carry in f64, the affine maps in
 // Affine<double>); per-element work always stays in S.
+//
+// kWide = true additionally runs the WHOLE scan / ordered reduction in C (f32
+// only at the boundary).  The menu uses it for product-type operators (affine
+// maps, quaternions): every one of the n-1 multiplications of a product chain
+// contributes its rounding error to the result whatever the tree shape, so an
+// f32 evaluation drifts like sqrt(n)*eps (the reference's own f32 fold shows
+// 1e-5 relative at n = 1e5); in f64 the result is within a few ulp of f32.
 template <class S, class Op, class = void>
 struct CarryTraits {
   using C = S;
+  static constexpr bool kWide = false;
   static __device__ __forceinline__ C to_c(const S& s) { return s; }
   static __device__ __forceinline__ S to_s(const C& c) { return c; }
   static __device__ __forceinline__ C op(const Op& o, const C& a, const C& b) { return o(a, b); }
@@ -41,6 +49,33 @@ struct CarryTraits {
 
 template <class S, class Op>
 struct CarryTraits<S, Op, std::void_t<typename Op::carry_traits>> : Op::carry_traits {};
+
+// Arithmetic of one scan / ordered reduction: values of type A live in
+// registers and shared memory; lift() maps f's S result in, lower() maps out,
+// to_c()/from_c() cross into the carry type.
+template <class S, class Op, bool Wide = CarryTraits<S, Op>::kWide>
+struct ScanMath {
+  using CT = CarryTraits<S, Op>;
+  using C = typename CT::C;
+  using A = S;
+  static __device__ __forceinline__ A lift(const S& s) { return s; }
+  static __device__ __forceinline__ S lower(const A& a) { return a; }
+  static __device__ __forceinline__ A comb(const Op& o, const A& x, const A& y) { return o(x, y); }
+  static __device__ __forceinline__ C to_c(const A& a) { return CT::to_c(a); }
+  static __device__ __forceinline__ A from_c(const C& c) { return CT::to_s(c); }
+};
+
+template <class S, class Op>
+struct ScanMath<S, Op, true> {
+  using CT = CarryTraits<S, Op>;
+  using C = typename CT::C;
+  using A = C;
+  static __device__ __forceinline__ A lift(const S& s) { return CT::to_c(s); }
+  static __device__ __forceinline__ S lower(const A& a) { return CT::to_s(a); }
+  static __device__ __forceinline__ A comb(const Op& o, const A& x, const A& y) { return CT::op(o, x, y); }
+  static __device__ __forceinline__ C to_c(const A& a) { return a; }
+  static __device__ __forceinline__ A from_c(const C& c) { return c; }
+};
 
 template <class T>
 constexpr int mr_vec_elems() {
@@ -292,14 +327,16 @@ struct OrderedReduceArgs {
 template <class T, class S, class F, class Op>
 __global__ void __launch_bounds__(kReduceThreads)
     reduce_ordered_kernel(const OrderedReduceArgs<T, S, F, Op, typename CarryTraits<S, Op>::C> a) {
-  using CT = CarryTraits<S, Op>;
+  using M = ScanMath<S, Op>;
+  using CT = typename M::CT;
   using C = typename CT::C;
+  using A = typename M::A;
   constexpr int IT = tile_items<T, S>();
   constexpr uint64_t kTile = uint64_t(kReduceThreads) * IT;
-  __shared__ Opt<S> smem[kReduceThreads / kWarp];
-  __shared__ Opt<C> csmem[kWarp];
+  __shared__ Opt<A> smem[kReduceThreads / kWarp];
   __shared__ bool s_last;
   auto cop = [&](const C& x, const C& y) { return CT::op(a.op, x, y); };
+  auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
 
   const uint64_t ntiles = ceil_div(a.n, kTile);
   const uint64_t t0 = uint64_t(blockIdx.x) * a.tiles_per_block;
@@ -308,22 +345,22 @@ __global__ void __launch_bounds__(kReduceThreads)
   Opt<C> bacc{C{}, false};  // meaningful in thread 0
   for (uint64_t t = t0; t < t1; ++t) {
     const uint64_t base = t * kTile + uint64_t(threadIdx.x) * IT;
-    Opt<S> mine{S{}, false};
+    Opt<A> mine{A{}, false};
     if (base + IT <= a.n && vec_ok) {
       T x[IT];
       load_items<T, IT>(a.src + base, x);
-      S v = a.f(x[0]);
+      A v = M::lift(a.f(x[0]));
 #pragma unroll
-      for (int k = 1; k < IT; ++k) v = a.op(v, a.f(x[k]));
-      mine = Opt<S>{v, true};
+      for (int k = 1; k < IT; ++k) v = aop(v, M::lift(a.f(x[k])));
+      mine = Opt<A>{v, true};
     } else {
       for (int k = 0; k < IT; ++k) {
-        if (base + k < a.n) mine = opt_combine(a.op, mine, Opt<S>{a.f(a.src[(base + k) * a.stride]), true});
+        if (base + k < a.n) mine = opt_combine(aop, mine, Opt<A>{M::lift(a.f(a.src[(base + k) * a.stride])), true});
       }
     }
-    Opt<S> tile = block_reduce_ordered(a.op, mine, smem);
+    Opt<A> tile = block_reduce_ordered(aop, mine, smem);
     if (threadIdx.x == 0 && tile.has) {
-      C tc = CT::to_c(tile.v);
+      C tc = M::to_c(tile.v);
       bacc = bacc.has ? Opt<C>{cop(bacc.v, tc), true} : Opt<C>{tc, true};
     }
   }
@@ -354,7 +391,6 @@ __global__ void __launch_bounds__(kReduceThreads)
     *a.out = CT::to_s(v.v);
     if (a.out_has) *a.out_has = v.has ? 1u : 0u;
   }
-  (void)csmem;
 }
 
 template <class S, class Op>

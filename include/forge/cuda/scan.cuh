@@ -1,31 +1,42 @@
 // forge/cuda/scan.cuh — single-pass decoupled look-back scan for sm_100a.
 //
-// Reference: prim::scan (primitives.hpp:440-603).  Same protocol, re-designed
-// for real hardware:
-//   * tile = 256 threads x IT items (IT = 64 B / max(sizeof T, sizeof S), <= 16:
-//     4096 f32, 2048 8-byte structs, 1024 16-byte structs); each thread loads
-//     its IT contiguous items with 256-bit ld.global.nc.v8 (primitives.hpp:486-498
-//     did a 16-wide vload per thread) and runs a register scan;
+// Reference: prim::scan (primitives.hpp:440-603).  Same protocol (tile
+// aggregate published as PARTIAL, look-back over predecessors until a PREFIX,
+// own PREFIX published, outputs composed in registers and stored once),
+// re-designed for real hardware:
+//   * tile = 256 threads x IT items, IT = 64 B / sizeof(S) (<= 16): 4096 f32,
+//     2048 eight-byte structs, 1024 sixteen-byte structs;
 //   * tile ids come from an atomic ticket, not blockIdx.x (the VM admitted
-//     blocks in id order, machine.cpp:767-776; CUDA does not guarantee that, so
-//     a tile could otherwise spin on a predecessor that is not resident);
-//   * tile status: every 32-bit chunk of the published carry travels in its own
-//     64-bit word {status, chunk}; a reader accepts a state only when all words
-//     carry the same status, so no fence and no separate flag byte are needed
-//     (the reference used a relaxed aggregate store + release flag,
+//     blocks in id order, machine.cpp:767-776; CUDA guarantees no such order,
+//     so a tile could otherwise spin on a predecessor that never becomes
+//     resident);
+//   * tile status: every 32-bit chunk of the published value travels in its
+//     own 64-bit word {status, chunk}; a reader accepts a state only when all
+//     words carry the same status, so no fence and no separate flag byte are
+//     needed (the reference: relaxed aggregate store + release flag,
 //     primitives.hpp:518-534, 568-575);
-//   * status = (epoch << 2) | {1 PARTIAL, 2 PREFIX}; the epoch advances at the
-//     end of every launch (the last tile to finish its look-back bumps it), so
-//     stale states of earlier launches read as INVALID and the workspace needs
-//     no fill_zero per launch (primitives.hpp:464-466);
+//   * status = (epoch << 2) | {1 PARTIAL, 2 PREFIX}; the last tile to finish
+//     its look-back advances the epoch, so stale states of earlier launches read
+//     as INVALID and the workspace needs no fill_zero per launch
+//     (primitives.hpp:464-466);
 //   * look-back: warp 0 polls 32 predecessors at once, finds the nearest PREFIX
 //     with one ballot and folds the window with a log-step ORDER-PRESERVING
-//     reduction (the reference folded the window serially with 32 shuffles,
-//     primitives.hpp:561-563);
-//   * the inter-tile carry chain runs in CarryTraits<S,Op>::C (f64 for the f32
-//     sums), per-element work in S;
-//   * optional carry_in (the exclusive prefix of earlier shards, sharded scan)
-//     and total_out (the inclusive total) device operands.
+//     reduction (the reference folded it serially, primitives.hpp:561-563);
+//   * inter-tile carries run in CarryTraits<S,Op>::C (f64 for the f32 sums);
+//     product-type ops run entirely in C (ScanMath, reduce.cuh);
+//   * optional carry_in (exclusive prefix of earlier shards) and total_out.
+//
+// Two kernels share the tile code:
+//   scan_tma_kernel      contiguous 16-B-aligned input: PERSISTENT CTAs (grid =
+//                        #SM x occupancy); each CTA claims tiles in ticket order
+//                        and keeps STAGES future tiles in flight with 1-D TMA
+//                        bulk copies (cp.async.bulk + mbarrier) into shared
+//                        memory, so HBM reads overlap the look-back and the
+//                        stores of the current tile.  Shared-memory reads use a
+//                        per-thread chunk rotation that makes the 64-byte-per-
+//                        thread blocked read conflict-free.
+//   scan_kernel          everything else (strided views, unaligned bases):
+//                        one tile per CTA, direct vector / scalar loads.
 #pragma once
 
 #include "forge/cuda/reduce.cuh"
@@ -33,7 +44,9 @@
 namespace forge::cuda {
 
 constexpr int kScanThreads = 256;
+constexpr int kScanStages = 3;
 constexpr uint32_t kPartial = 1, kPrefix = 2;
+constexpr uint32_t kNoTile = 0xffffffffu;
 
 template <class C>
 struct TileStateIO {
@@ -50,9 +63,9 @@ struct TileStateIO {
     } else {
 #pragma unroll
       for (int i = 0; i < STRIDE; i += 2) {
-        const uint64_t a = hi | (i < SW ? w.w[i] : 0u);
-        const uint64_t b = hi | (i + 1 < SW ? w.w[i + 1] : 0u);
-        st_relaxed_gpu_v2(p + i, a, b);
+        const uint64_t lo_word = hi | (i < SW ? w.w[i] : 0u);
+        const uint64_t hi_word = hi | (i + 1 < SW ? w.w[i + 1] : 0u);
+        st_relaxed_gpu_v2(p + i, lo_word, hi_word);
       }
     }
   }
@@ -90,89 +103,80 @@ struct ScanArgs {
   uint64_t src_stride, dst_stride;
   F f;
   Op op;
-  S identity;          // exclusive output at index 0 when there is no carry-in
-  const S* carry_in;   // nullable, device
-  S* total_out;        // nullable, device
-  uint64_t* states;    // [ntiles * STRIDE] 64-bit words
-  uint32_t* ctrl;      // [0] ticket, [1] done counter, [2] epoch
+  S identity;         // exclusive output at index 0 when there is no carry-in
+  const S* carry_in;  // nullable, device
+  S* total_out;       // nullable, device
+  uint64_t* states;   // [ntiles * STRIDE] 64-bit words
+  uint32_t* ctrl;     // [0] ticket, [1] done counter, [2] epoch
   uint32_t ntiles;
 };
 
-template <class T, class S, class F, class Op, bool Inclusive>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S, F, Op> a) {
-  using CT = CarryTraits<S, Op>;
-  using C = typename CT::C;
+// Per-CTA shared state of one tile.
+template <class A>
+struct ScanShared {
+  Opt<A> warp[kScanThreads / kWarp];
+  Opt<A> carry;
+};
+
+// Everything after the items are in registers: register scan, block scan,
+// publish + look-back, compose, store.  `raw` holds this thread's IT input
+// items; `count` how many are valid.
+template <class T, class S, class F, class Op, bool Inclusive, int IT>
+__device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, uint64_t tile,
+                                               uint32_t epoch, const T (&raw)[IT], int count,
+                                               ScanShared<typename ScanMath<S, Op>::A>& sh) {
+  using M = ScanMath<S, Op>;
+  using A = typename M::A;
+  using C = typename M::C;
   using IO = TileStateIO<C>;
-  constexpr int IT = scan_items<S>();
-  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
   constexpr int NW = kScanThreads / kWarp;
-
-  __shared__ uint32_t s_tile, s_epoch;
-  __shared__ Opt<S> s_warp[NW];
-  __shared__ Opt<S> s_carry;
-
+  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
   const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
-  if (threadIdx.x == 0) {
-    const uint32_t t = atom_add_relaxed_gpu(a.ctrl + 0, 1u);
-    if (t == a.ntiles - 1) st_relaxed_gpu(a.ctrl + 0, 0u);  // all tiles claimed
-    s_tile = t;
-    s_epoch = ld_acquire_gpu(a.ctrl + 2);
-  }
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint32_t epoch = s_epoch;
+  auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
+  auto cop = [&](const C& x, const C& y) { return M::CT::op(a.op, x, y); };
 
-  // ---- load + per-thread register scan (primitives.hpp:484-499)
-  const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * IT;
-  const uint64_t avail = base < a.n ? a.n - base : 0;
-  const int count = avail >= uint64_t(IT) ? IT : int(avail);
-  S regs[IT];
-  if (count == IT && a.src_stride == 1 && is_aligned(a.src + base, items_align<T, IT>())) {
-    T x[IT];
-    load_items<T, IT>(a.src + base, x);
-    regs[0] = a.f(x[0]);
+  // ---- per-thread register scan (primitives.hpp:484-499)
+  A regs[IT];
 #pragma unroll
-    for (int k = 1; k < IT; ++k) regs[k] = a.op(regs[k - 1], a.f(x[k]));
-  } else {
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      if (k < count) {
-        S v = a.f(a.src[(base + k) * a.src_stride]);
-        regs[k] = k ? a.op(regs[k - 1], v) : v;
-      }
+  for (int k = 0; k < IT; ++k) {
+    if (k < count) {
+      const A v = M::lift(a.f(raw[k]));
+      regs[k] = k ? aop(regs[k - 1], v) : v;
     }
   }
-  S last = regs[0];
+  A last = regs[0];
 #pragma unroll
   for (int k = 1; k < IT; ++k)
     if (k < count) last = regs[k];
 
-  // ---- warp scan, then cross-warp scan through shared memory (:501-516)
-  const Opt<S> incl = warp_scan_incl(a.op, Opt<S>{last, count > 0});
-  if (lane == kWarp - 1) s_warp[warp] = incl;
+  // ---- warp scan, cross-warp scan through shared memory (:501-516)
+  const Opt<A> incl = warp_scan_incl(aop, Opt<A>{last, count > 0});
+  if (lane == kWarp - 1) sh.warp[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    Opt<S> w = lane < NW ? s_warp[lane] : Opt<S>{S{}, false};
-    w = warp_scan_incl(a.op, w);
-    if (lane < NW) s_warp[lane] = w;
+    Opt<A> w = lane < NW ? sh.warp[lane] : Opt<A>{A{}, false};
+    w = warp_scan_incl(aop, w);
+    if (lane < NW) sh.warp[lane] = w;
   }
   __syncthreads();
-  const Opt<S> agg = s_warp[NW - 1];  // tile aggregate (a tile always holds >= 1 element)
+  const Opt<A> agg = sh.warp[NW - 1];  // every tile holds >= 1 element
 
   // ---- publish + decoupled look-back (:518-576)
   if (tile == 0) {
     if (threadIdx.x == 0) {
-      Opt<S> cin = a.carry_in ? Opt<S>{*a.carry_in, true} : Opt<S>{S{}, false};
-      C pre = CT::to_c(agg.v);
-      if (cin.has) pre = CT::op(a.op, CT::to_c(cin.v), pre);
+      C pre = M::to_c(agg.v);
+      Opt<A> cin{A{}, false};
+      if (a.carry_in) {
+        cin = Opt<A>{M::lift(*a.carry_in), true};
+        pre = cop(M::to_c(cin.v), pre);
+      }
       IO::write(a.states, 0, epoch, kPrefix, pre);
-      s_carry = cin;
-      if (a.ntiles == 1 && a.total_out) *a.total_out = CT::to_s(pre);
+      sh.carry = cin;
+      if (a.ntiles == 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
     }
   } else if (warp == 0) {
-    const C agg_c = CT::to_c(agg.v);
+    const C agg_c = M::to_c(agg.v);
     if (lane == 0) IO::write(a.states, tile, epoch, kPartial, agg_c);
-    auto cop = [&](const C& x, const C& y) { return CT::op(a.op, x, y); };
     Opt<C> carry{C{}, false};
     int64_t hi = int64_t(tile);
     for (;;) {
@@ -185,8 +189,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
       }
       const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
       const int pl = pm ? __ffs(int(pm)) - 1 : kWarp - 1;
-      // Lanes 0..pl hold tiles hi-1 .. hi-1-pl (newest first); fold them with the
-      // older (higher) lane on the LEFT of every combine.
+      // Lanes 0..pl hold tiles hi-1 .. hi-1-pl (newest first): fold them with
+      // the older (higher) lane on the LEFT of every combine.
       Opt<C> v{val, int(lane) <= pl && j >= 0};
 #pragma unroll
       for (unsigned d = 1; d < kWarp; d <<= 1) {
@@ -201,8 +205,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
     if (lane == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
       IO::write(a.states, tile, epoch, kPrefix, inclusive_c);
-      s_carry = Opt<S>{CT::to_s(carry.v), true};
-      if (tile == a.ntiles - 1 && a.total_out) *a.total_out = CT::to_s(inclusive_c);
+      sh.carry = Opt<A>{M::from_c(carry.v), true};
+      if (tile == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(inclusive_c);
     }
   }
   __syncthreads();
@@ -218,20 +222,21 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
   }
 
   // ---- compose outputs in registers and store once (:579-600)
-  const Opt<S> tile_ex = s_carry;
-  const Opt<S> warp_ex = warp > 0 ? s_warp[warp - 1] : Opt<S>{S{}, false};
-  Opt<S> lane_ex = shfl_up_opt(incl, 1);
+  const Opt<A> tile_ex = sh.carry;
+  const Opt<A> warp_ex = warp > 0 ? sh.warp[warp - 1] : Opt<A>{A{}, false};
+  Opt<A> lane_ex = shfl_up_opt(incl, 1);
   if (lane == 0) lane_ex.has = false;
-  const Opt<S> pre = opt_combine(a.op, opt_combine(a.op, tile_ex, warp_ex), lane_ex);
+  const Opt<A> pre = opt_combine(aop, opt_combine(aop, tile_ex, warp_ex), lane_ex);
   if (count == 0) return;
+  const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * IT;
   S outs[IT];
   if constexpr (Inclusive) {
 #pragma unroll
-    for (int k = 0; k < IT; ++k) outs[k] = pre.has ? a.op(pre.v, regs[k]) : regs[k];
+    for (int k = 0; k < IT; ++k) outs[k] = M::lower(pre.has ? aop(pre.v, regs[k]) : regs[k]);
   } else {
-    outs[0] = pre.has ? pre.v : a.identity;
+    outs[0] = pre.has ? M::lower(pre.v) : a.identity;
 #pragma unroll
-    for (int k = 1; k < IT; ++k) outs[k] = pre.has ? a.op(pre.v, regs[k - 1]) : regs[k - 1];
+    for (int k = 1; k < IT; ++k) outs[k] = M::lower(pre.has ? aop(pre.v, regs[k - 1]) : regs[k - 1]);
   }
   if (count == IT && a.dst_stride == 1 && is_aligned(a.dst + base, items_align<S, IT>())) {
     store_items<S, IT>(a.dst + base, outs);
@@ -239,6 +244,162 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
 #pragma unroll
     for (int k = 0; k < IT; ++k)
       if (k < count) a.dst[(base + k) * a.dst_stride] = outs[k];
+  }
+}
+
+template <class T, int IT>
+__device__ __forceinline__ int load_tile_items_global(const T* src, uint64_t stride, uint64_t n,
+                                                      uint64_t base, T (&raw)[IT]) {
+  const uint64_t avail = base < n ? n - base : 0;
+  const int count = avail >= uint64_t(IT) ? IT : int(avail);
+  if (count == IT && stride == 1 && is_aligned(src + base, items_align<T, IT>())) {
+    load_items<T, IT>(src + base, raw);
+  } else {
+#pragma unroll
+    for (int k = 0; k < IT; ++k)
+      if (k < count) raw[k] = src[(base + k) * stride];
+  }
+  return count;
+}
+
+// ---------------------------------------------------------------------------
+// General path: one tile per CTA.
+
+template <class T, class S, class F, class Op, bool Inclusive>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S, F, Op> a) {
+  using A = typename ScanMath<S, Op>::A;
+  constexpr int IT = scan_items<S>();
+  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
+  __shared__ uint32_t s_tile, s_epoch;
+  __shared__ ScanShared<A> sh;
+  if (threadIdx.x == 0) {
+    const uint32_t t = atom_add_relaxed_gpu(a.ctrl + 0, 1u);
+    if (t == a.ntiles - 1) st_relaxed_gpu(a.ctrl + 0, 0u);  // exactly ntiles claims
+    s_tile = t;
+    s_epoch = ld_acquire_gpu(a.ctrl + 2);
+  }
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  T raw[IT];
+  const int count =
+      load_tile_items_global<T, IT>(a.src, a.src_stride, a.n, tile * kTile + uint64_t(threadIdx.x) * IT, raw);
+  scan_tile_body<T, S, F, Op, Inclusive, IT>(a, tile, s_epoch, raw, count, sh);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent TMA-pipelined path (contiguous, 16-byte aligned input).
+
+// Reads IT items (IT * sizeof(T) bytes) of one thread from shared memory.  For
+// 64-byte rows the four 16-byte chunks are read in an order rotated by
+// (tid >> 1) & 3 — each quarter-warp phase then touches 8 distinct 16-byte bank
+// groups (conflict-free) — and put back in logical order with two conditional
+// swap stages.
+template <class T, int IT>
+__device__ __forceinline__ void load_items_smem(const T* row, T (&out)[IT]) {
+  constexpr int kBytes = IT * int(sizeof(T));
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(row);
+  if constexpr (kBytes == 64) {
+    const unsigned r = (threadIdx.x >> 1) & 3u;
+    uint4 c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = lds128(p + 16 * (k ^ r));
+    if (r & 1u) {
+      uint4 t = c[0]; c[0] = c[1]; c[1] = t;
+      t = c[2]; c[2] = c[3]; c[3] = t;
+    }
+    if (r & 2u) {
+      uint4 t = c[0]; c[0] = c[2]; c[2] = t;
+      t = c[1]; c[1] = c[3]; c[3] = t;
+    }
+    memcpy(out, c, 64);
+  } else if constexpr (kBytes % 16 == 0) {
+    uint4 c[kBytes / 16];
+#pragma unroll
+    for (int k = 0; k < kBytes / 16; ++k) c[k] = lds128(p + 16 * k);
+    memcpy(out, c, kBytes);
+  } else {
+#pragma unroll
+    for (int k = 0; k < IT; ++k) out[k] = row[k];
+  }
+}
+
+template <class T, class S>
+constexpr uint32_t scan_tile_bytes() {
+  return uint32_t(kScanThreads) * scan_items<S>() * uint32_t(sizeof(T));
+}
+
+template <class T, class S>
+constexpr bool scan_tma_eligible() {
+  return scan_tile_bytes<T, S>() % 16 == 0;
+}
+
+template <class T, class S, class F, class Op, bool Inclusive>
+__global__ void __launch_bounds__(kScanThreads) scan_tma_kernel(const ScanArgs<T, S, F, Op> a) {
+  using A = typename ScanMath<S, Op>::A;
+  constexpr int IT = scan_items<S>();
+  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
+  constexpr uint32_t kBytes = scan_tile_bytes<T, S>();
+  extern __shared__ __align__(128) unsigned char stage_mem[];
+  __shared__ __align__(8) uint64_t bars[kScanStages];
+  __shared__ uint32_t ring[kScanStages];
+  __shared__ uint32_t s_epoch;
+  __shared__ bool s_claim_open;
+  __shared__ ScanShared<A> sh;
+
+  // Thread 0 claims the next tile into stage s (ticket order) and starts its
+  // TMA.  Each CTA claims until its first failure, so a launch makes exactly
+  // ntiles + gridDim.x claims and the last one resets the ticket.
+  const bool tail_partial = (a.n % kTile) != 0;
+  auto claim = [&](int s) {
+    uint32_t t = kNoTile;
+    if (s_claim_open) {
+      t = atom_add_relaxed_gpu(a.ctrl + 0, 1u);
+      if (t == a.ntiles + gridDim.x - 1) st_relaxed_gpu(a.ctrl + 0, 0u);
+      if (t >= a.ntiles) {
+        s_claim_open = false;
+        t = kNoTile;
+      }
+    }
+    ring[s] = t;
+    if (t == kNoTile) return;
+    fence_proxy_async_smem();  // generic reads of the stage before the async-proxy refill
+    if (tail_partial && t == a.ntiles - 1) {
+      mbar_arrive(&bars[s]);  // partial last tile: threads read global memory directly
+    } else {
+      mbar_arrive_expect_tx(&bars[s], kBytes);
+      tma_load_1d(stage_mem + size_t(s) * kBytes, a.src + uint64_t(t) * kTile, kBytes, &bars[s]);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kScanStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    s_epoch = ld_acquire_gpu(a.ctrl + 2);
+    s_claim_open = true;
+    for (int s = 0; s < kScanStages; ++s) claim(s);
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+
+  for (uint32_t it = 0;; ++it) {
+    const int s = int(it % kScanStages);
+    const uint32_t phase = (it / kScanStages) & 1u;
+    const uint32_t tile = ring[s];
+    if (tile == kNoTile) break;
+    mbar_wait(&bars[s], phase);
+    T raw[IT];
+    int count;
+    const uint64_t base = uint64_t(tile) * kTile + uint64_t(threadIdx.x) * IT;
+    if (tail_partial && tile == a.ntiles - 1) {
+      count = load_tile_items_global<T, IT>(a.src, 1, a.n, base, raw);
+    } else {
+      load_items_smem<T, IT>(reinterpret_cast<const T*>(stage_mem + size_t(s) * kBytes) + threadIdx.x * IT, raw);
+      count = IT;
+    }
+    __syncthreads();                // stage s fully consumed, ring[s] read by all
+    if (threadIdx.x == 0) claim(s);  // refill it with this CTA's next ticket
+    scan_tile_body<T, S, F, Op, Inclusive, IT>(a, tile, epoch, raw, count, sh);
+    __syncthreads();  // sh reuse + ring visibility for the next iteration
   }
 }
 
@@ -252,6 +413,24 @@ struct ScanWs {
   }
 };
 
+template <class T, class S, class F, class Op, bool Inclusive>
+inline uint32_t scan_tma_grid(uint64_t ntiles) {
+  static thread_local int cached_dev = -1, cached_occ = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    const size_t smem = size_t(kScanStages) * scan_tile_bytes<T, S>();
+    cudaFuncSetAttribute(scan_tma_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_tma_kernel<T, S, F, Op, Inclusive>, kScanThreads, smem);
+    cached_occ = occ < 1 ? 1 : occ;
+    cached_dev = dev;
+  }
+  const uint64_t cap = uint64_t(device_props().sm_count) * cached_occ;
+  return uint32_t(ntiles < cap ? ntiles : cap);
+}
+
 template <class T, class S, class F, class Op>
 cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_stride, uint64_t n,
                         bool inclusive, const F& f, const Op& op, const S& identity,
@@ -259,14 +438,25 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   const uint64_t ntiles = ScanWs<T, S, Op>::tiles(n);
   if (ntiles == 0) return cudaSuccess;
   if (ntiles >= (1ull << 31)) return cudaErrorInvalidValue;
-  ScanArgs<T, S, F, Op> a{src,      dst,       n,   src_stride, dst_stride,
-                          f,        op,        identity, carry_in, total_out,
+  ScanArgs<T, S, F, Op> a{src,      dst,       n,         src_stride, dst_stride,
+                          f,        op,        identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
                           static_cast<uint32_t*>(ws), uint32_t(ntiles)};
-  if (inclusive)
-    scan_kernel<T, S, F, Op, true><<<uint32_t(ntiles), kScanThreads, 0, stream>>>(a);
-  else
-    scan_kernel<T, S, F, Op, false><<<uint32_t(ntiles), kScanThreads, 0, stream>>>(a);
+  const bool tma = scan_tma_eligible<T, S>() && src_stride == 1 && is_aligned(src, 16) && ntiles >= 2;
+  if (tma) {
+    const size_t smem = size_t(kScanStages) * scan_tile_bytes<T, S>();
+    if (inclusive)
+      scan_tma_kernel<T, S, F, Op, true>
+          <<<scan_tma_grid<T, S, F, Op, true>(ntiles), kScanThreads, smem, stream>>>(a);
+    else
+      scan_tma_kernel<T, S, F, Op, false>
+          <<<scan_tma_grid<T, S, F, Op, false>(ntiles), kScanThreads, smem, stream>>>(a);
+  } else {
+    if (inclusive)
+      scan_kernel<T, S, F, Op, true><<<uint32_t(ntiles), kScanThreads, 0, stream>>>(a);
+    else
+      scan_kernel<T, S, F, Op, false><<<uint32_t(ntiles), kScanThreads, 0, stream>>>(a);
+  }
   return cudaGetLastError();
 }
 

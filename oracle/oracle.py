@@ -85,7 +85,15 @@ def ref() -> C.CDLL:
 
 
 def _ptr(a) -> C.c_void_p:
-    return a.ctypes.data_as(C.c_void_p) if a is not None else C.c_void_p(0)
+    if a is None:
+        return C.c_void_p(0)
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("oracle inputs must be C-contiguous (use np.ascontiguousarray)")
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _c(a):
+    return None if a is None else np.ascontiguousarray(a)
 
 
 # ---- dtype table (mirrors paper_2603_18695_b200.forge._TYPES, kept separate so
@@ -120,6 +128,7 @@ def fill(op, n, seed, variant=0, index_base=0) -> np.ndarray:
 
 def mapreduce(op, src: np.ndarray, stride: int = 1):
     """Returns (S value, exact[ncomp], scale[ncomp])."""
+    src = _c(src)
     nc = max(ncomp(op), 1)
     out = np.zeros(1, dtype=s_dtype(op))
     ex, sc = np.zeros(nc), np.zeros(nc)
@@ -138,6 +147,7 @@ def mapreduce_synthetic(op, n, seed, variant=0):
 
 def scan(op, inclusive: bool, src: np.ndarray, carry=None):
     """Returns (dst S array, exact[n, ncomp], scale[n, ncomp])."""
+    src = _c(src)
     n = len(src)
     nc = max(ncomp(op), 1)
     dst = np.zeros(n, dtype=s_dtype(op))
@@ -150,6 +160,7 @@ def scan(op, inclusive: bool, src: np.ndarray, carry=None):
 
 
 def matvec(op, A: np.ndarray, n, p, x=None):
+    A, x = _c(A), _c(x)
     nc = max(ncomp(op), 1)
     y = np.zeros(p, dtype=s_dtype(op))
     ex, sc = np.zeros((p, nc)), np.zeros((p, nc))
@@ -158,6 +169,7 @@ def matvec(op, A: np.ndarray, n, p, x=None):
 
 
 def vecmat(op, A: np.ndarray, n, p, x=None):
+    A, x = _c(A), _c(x)
     nc = max(ncomp(op), 1)
     z = np.zeros(n, dtype=s_dtype(op))
     ex, sc = np.zeros((n, nc)), np.zeros((n, nc))
@@ -175,6 +187,7 @@ def vload_pattern(offset, nitem):
 
 
 def check_scan_synthetic(op, inclusive, n, seed, got: np.ndarray, tol: float, variant=0):
+    got = _c(got)
     worst = C.c_double()
     bad = lib().orc_check_scan_synthetic(op, 1 if inclusive else 0, n, seed, variant, _ptr(got), tol,
                                          C.byref(worst))
@@ -192,7 +205,9 @@ def float_view(op, arr: np.ndarray) -> np.ndarray:
 def within(op, got: np.ndarray, exact: np.ndarray, scale: np.ndarray, tol: float) -> tuple[bool, float]:
     """|got - exact| <= tol * scale component-wise (SURVEY.md §8(c) parity rule)."""
     g = float_view(op, got)
-    err = np.abs(g - exact.reshape(g.shape))
+    e = exact.reshape(g.shape)
+    with np.errstate(invalid="ignore"):
+        err = np.where(g == e, 0.0, np.abs(g - e))  # equal infinities (identities) are exact
     sc = scale.reshape(g.shape)
     ok = np.all(err <= tol * sc) and np.all(np.isfinite(g) == np.isfinite(exact.reshape(g.shape)))
     rel = float(np.max(np.where(sc > 0, err / np.where(sc > 0, sc, 1), np.where(err > 0, np.inf, 0)))) if g.size else 0.0

@@ -21,6 +21,7 @@ using namespace forge::alg;
 // ---- carry policies
 struct F32SumCarry {
   using C = double;
+  static constexpr bool kWide = false;  // sums: f32 per element, f64 across tiles
   static __device__ __forceinline__ C to_c(float s) { return double(s); }
   static __device__ __forceinline__ float to_s(C c) { return float(c); }
   template <class Op>
@@ -29,6 +30,7 @@ struct F32SumCarry {
 
 struct AffineCarry {
   using C = AffineT<double>;
+  static constexpr bool kWide = true;  // product chain: whole scan in f64
   static __device__ __forceinline__ C to_c(const Affine& s) { return C{double(s.a), double(s.b)}; }
   static __device__ __forceinline__ Affine to_s(const C& c) { return Affine{float(c.a), float(c.b)}; }
   template <class Op>
@@ -40,6 +42,7 @@ struct QuatD {
 };
 struct QuatCarry {
   using C = QuatD;
+  static constexpr bool kWide = true;  // product chain: whole scan in f64
   static __device__ __forceinline__ C to_c(const Quaternion& q) { return C{q.w, q.x, q.y, q.z}; }
   static __device__ __forceinline__ Quaternion to_s(const C& c) {
     return Quaternion{float(c.w), float(c.x), float(c.y), float(c.z)};
@@ -53,6 +56,7 @@ struct QuatCarry {
 
 struct LseCarry {
   using C = double;
+  static constexpr bool kWide = false;
   static __device__ __forceinline__ C to_c(float s) { return double(s); }
   static __device__ __forceinline__ float to_s(C c) { return float(c); }
   template <class Op>

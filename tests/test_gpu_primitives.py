@@ -194,6 +194,25 @@ def test_scan_workspace_reuse_epochs(m):
         m.destroy_buffer(d)
 
 
+def test_scan_mixed_paths_share_workspace(m):
+    # The persistent TMA kernel (aligned contiguous input) and the general
+    # kernel (misaligned / strided) alternate on ONE workspace: ticket, done
+    # counter and epoch must stay consistent across both.
+    op = F.I32_SUM
+    n_all = 250_001
+    x = orc.fill(op, n_all, 4242)
+    a = upload(m, op, x)
+    d = F.create_buffer(m, op, n_all, which="S")
+    ws = F.make_scan_workspace(m, op, n_all)
+    for k in range(10):
+        off = 0 if k % 2 == 0 else 1 + k
+        cnt = n_all - off - (k * 997)
+        F.scan(m, F.make_semiring(op), F.View(a, off, cnt, 1), F.View(d, off, cnt, 1), k % 3 != 0, ws)
+        got = m.read(d, n_all, np.int32)[off:off + cnt]
+        want, _, _ = orc.scan(op, k % 3 != 0, x[off:off + cnt])
+        assert np.array_equal(got, want), f"launch {k}"
+
+
 def test_scan_noncommutative_mat2_exact(m):
     # 2x2 wrapping-integer matrix scan equals the sequential oracle exactly.
     op = F.MAT2_U32
