@@ -111,6 +111,12 @@ struct ScanArgs {
   uint32_t ntiles;
 };
 
+// The 256 consumer threads synchronise on named barrier 1, so a producer warp
+// outside the barrier never stalls them (and vice versa).
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kScanThreads) : "memory");
+}
+
 // Per-CTA shared state of one tile.
 template <class A>
 struct ScanShared {
@@ -152,13 +158,13 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
   // ---- warp scan, cross-warp scan through shared memory (:501-516)
   const Opt<A> incl = warp_scan_incl(aop, Opt<A>{last, count > 0});
   if (lane == kWarp - 1) sh.warp[warp] = incl;
-  __syncthreads();
+  consumer_sync();
   if (warp == 0) {
     Opt<A> w = lane < NW ? sh.warp[lane] : Opt<A>{A{}, false};
     w = warp_scan_incl(aop, w);
     if (lane < NW) sh.warp[lane] = w;
   }
-  __syncthreads();
+  consumer_sync();
   const Opt<A> agg = sh.warp[NW - 1];  // every tile holds >= 1 element
 
   // ---- publish + decoupled look-back (:518-576)
@@ -209,17 +215,7 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
       if (tile == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(inclusive_c);
     }
   }
-  __syncthreads();
-
-  // This tile has finished reading predecessor states: count it; the last one
-  // advances the epoch for the next launch and resets the counter.
-  if (threadIdx.x == 0) {
-    const uint32_t d = atom_add_acq_rel_gpu(a.ctrl + 1, 1u);
-    if (d == a.ntiles - 1) {
-      st_relaxed_gpu(a.ctrl + 1, 0u);
-      st_relaxed_gpu(a.ctrl + 2, epoch + 1u);
-    }
-  }
+  consumer_sync();
 
   // ---- compose outputs in registers and store once (:579-600)
   const Opt<A> tile_ex = sh.carry;
@@ -273,10 +269,16 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
   __shared__ uint32_t s_tile, s_epoch;
   __shared__ ScanShared<A> sh;
   if (threadIdx.x == 0) {
-    const uint32_t t = atom_add_relaxed_gpu(a.ctrl + 0, 1u);
-    if (t == a.ntiles - 1) st_relaxed_gpu(a.ctrl + 0, 0u);  // exactly ntiles claims
-    s_tile = t;
+    // Epoch first, then the acq_rel claim: every CTA's epoch read happens
+    // before the last claim, whose owner may then advance the epoch for the
+    // NEXT launch (this launch keeps using the value each CTA cached).
     s_epoch = ld_acquire_gpu(a.ctrl + 2);
+    const uint32_t t = atom_add_acq_rel_gpu(a.ctrl + 0, 1u);
+    if (t == a.ntiles - 1) {  // exactly ntiles claims: this is the last one
+      st_relaxed_gpu(a.ctrl + 0, 0u);
+      st_relaxed_gpu(a.ctrl + 2, s_epoch + 1u);
+    }
+    s_tile = t;
   }
   __syncthreads();
   const uint64_t tile = s_tile;
@@ -333,60 +335,70 @@ constexpr bool scan_tma_eligible() {
   return scan_tile_bytes<T, S>() % 16 == 0;
 }
 
+constexpr int kScanProducerThreads = 32;  // one producer warp (lane 0 works)
+constexpr int kScanTmaThreads = kScanThreads + kScanProducerThreads;
+
 template <class T, class S, class F, class Op, bool Inclusive>
-__global__ void __launch_bounds__(kScanThreads) scan_tma_kernel(const ScanArgs<T, S, F, Op> a) {
+__global__ void __launch_bounds__(kScanTmaThreads) scan_tma_kernel(const ScanArgs<T, S, F, Op> a) {
   using A = typename ScanMath<S, Op>::A;
   constexpr int IT = scan_items<S>();
   constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
   constexpr uint32_t kBytes = scan_tile_bytes<T, S>();
+  constexpr int NW = kScanThreads / kWarp;
   extern __shared__ __align__(128) unsigned char stage_mem[];
-  __shared__ __align__(8) uint64_t bars[kScanStages];
+  __shared__ __align__(8) uint64_t full[kScanStages];   // TMA landed (count 1 + tx)
+  __shared__ __align__(8) uint64_t empty[kScanStages];  // consumers done (count NW)
   __shared__ uint32_t ring[kScanStages];
   __shared__ uint32_t s_epoch;
-  __shared__ bool s_claim_open;
   __shared__ ScanShared<A> sh;
 
-  // Thread 0 claims the next tile into stage s (ticket order) and starts its
-  // TMA.  Each CTA claims until its first failure, so a launch makes exactly
-  // ntiles + gridDim.x claims and the last one resets the ticket.
   const bool tail_partial = (a.n % kTile) != 0;
-  auto claim = [&](int s) {
-    uint32_t t = kNoTile;
-    if (s_claim_open) {
-      t = atom_add_relaxed_gpu(a.ctrl + 0, 1u);
-      if (t == a.ntiles + gridDim.x - 1) st_relaxed_gpu(a.ctrl + 0, 0u);
-      if (t >= a.ntiles) {
-        s_claim_open = false;
-        t = kNoTile;
-      }
+  if (threadIdx.x == kScanThreads) {
+    for (int s = 0; s < kScanStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
     }
-    ring[s] = t;
-    if (t == kNoTile) return;
-    fence_proxy_async_smem();  // generic reads of the stage before the async-proxy refill
-    if (tail_partial && t == a.ntiles - 1) {
-      mbar_arrive(&bars[s]);  // partial last tile: threads read global memory directly
-    } else {
-      mbar_arrive_expect_tx(&bars[s], kBytes);
-      tma_load_1d(stage_mem + size_t(s) * kBytes, a.src + uint64_t(t) * kTile, kBytes, &bars[s]);
-    }
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kScanStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    s_epoch = ld_acquire_gpu(a.ctrl + 2);
-    s_claim_open = true;
-    for (int s = 0; s < kScanStages; ++s) claim(s);
   }
   __syncthreads();
-  const uint32_t epoch = s_epoch;
 
+  if (threadIdx.x >= kScanThreads) {
+    // ---- producer warp: claims tiles in ticket order and keeps kScanStages
+    // of them in flight.  The epoch is read BEFORE the first (acq_rel) claim;
+    // each CTA claims until its first failure, so a launch makes exactly
+    // ntiles + gridDim.x claims, and the last claimer resets the ticket and
+    // advances the epoch for the next launch.
+    if (threadIdx.x != kScanThreads) return;
+    const uint32_t epoch = ld_acquire_gpu(a.ctrl + 2);
+    s_epoch = epoch;
+    for (uint32_t it = 0;; ++it) {
+      const int s = int(it % kScanStages);
+      if (it >= uint32_t(kScanStages)) mbar_wait(&empty[s], ((it / kScanStages) - 1) & 1u);
+      uint32_t t = atom_add_acq_rel_gpu(a.ctrl + 0, 1u);
+      if (t == a.ntiles + gridDim.x - 1) {
+        st_relaxed_gpu(a.ctrl + 0, 0u);
+        st_relaxed_gpu(a.ctrl + 2, epoch + 1u);
+      }
+      if (t >= a.ntiles) t = kNoTile;
+      ring[s] = t;
+      if (t != kNoTile && !(tail_partial && t == a.ntiles - 1)) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[s], kBytes);
+        tma_load_1d(stage_mem + size_t(s) * kBytes, a.src + uint64_t(t) * kTile, kBytes, &full[s]);
+      } else {
+        mbar_arrive(&full[s]);  // end marker, or partial last tile read from global
+      }
+      if (t == kNoTile) return;
+    }
+  }
+
+  // ---- 8 consumer warps
   for (uint32_t it = 0;; ++it) {
     const int s = int(it % kScanStages);
-    const uint32_t phase = (it / kScanStages) & 1u;
+    mbar_wait(&full[s], (it / kScanStages) & 1u);
     const uint32_t tile = ring[s];
     if (tile == kNoTile) break;
-    mbar_wait(&bars[s], phase);
+    const uint32_t epoch = s_epoch;
     T raw[IT];
     int count;
     const uint64_t base = uint64_t(tile) * kTile + uint64_t(threadIdx.x) * IT;
@@ -396,10 +408,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_tma_kernel(const ScanArgs<T
       load_items_smem<T, IT>(reinterpret_cast<const T*>(stage_mem + size_t(s) * kBytes) + threadIdx.x * IT, raw);
       count = IT;
     }
-    __syncthreads();                // stage s fully consumed, ring[s] read by all
-    if (threadIdx.x == 0) claim(s);  // refill it with this CTA's next ticket
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     scan_tile_body<T, S, F, Op, Inclusive, IT>(a, tile, epoch, raw, count, sh);
-    __syncthreads();  // sh reuse + ring visibility for the next iteration
+    consumer_sync();  // `sh` is reused by the next tile
   }
 }
 
@@ -423,7 +435,7 @@ inline uint32_t scan_tma_grid(uint64_t ntiles) {
     cudaFuncSetAttribute(scan_tma_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_tma_kernel<T, S, F, Op, Inclusive>, kScanThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_tma_kernel<T, S, F, Op, Inclusive>, kScanTmaThreads, smem);
     cached_occ = occ < 1 ? 1 : occ;
     cached_dev = dev;
   }
@@ -447,10 +459,10 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
     const size_t smem = size_t(kScanStages) * scan_tile_bytes<T, S>();
     if (inclusive)
       scan_tma_kernel<T, S, F, Op, true>
-          <<<scan_tma_grid<T, S, F, Op, true>(ntiles), kScanThreads, smem, stream>>>(a);
+          <<<scan_tma_grid<T, S, F, Op, true>(ntiles), kScanTmaThreads, smem, stream>>>(a);
     else
       scan_tma_kernel<T, S, F, Op, false>
-          <<<scan_tma_grid<T, S, F, Op, false>(ntiles), kScanThreads, smem, stream>>>(a);
+          <<<scan_tma_grid<T, S, F, Op, false>(ntiles), kScanTmaThreads, smem, stream>>>(a);
   } else {
     if (inclusive)
       scan_kernel<T, S, F, Op, true><<<uint32_t(ntiles), kScanThreads, 0, stream>>>(a);

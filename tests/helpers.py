@@ -25,7 +25,8 @@ def seed_for(*parts) -> int:
 def assert_match(op, got, want_s, exact, scale, what=""):
     """Exact ops: bitwise equality of the S values; float ops: tolerance."""
     nc = orc.ncomp(op)
-    got = np.atleast_1d(got)
+    got = np.ascontiguousarray(np.atleast_1d(got))
+    want_s = np.ascontiguousarray(np.atleast_1d(want_s))
     if nc == 0:
         g = got.view(np.uint8) if got.dtype.names is None else got.view(np.uint8)
         w = np.atleast_1d(want_s).view(np.uint8)
