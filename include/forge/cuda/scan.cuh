@@ -118,11 +118,16 @@ __device__ __forceinline__ void consumer_sync() {
 }
 
 // Per-CTA shared state of one tile.
-template <class A>
+template <class A, class C>
 struct ScanShared {
   Opt<A> warp[kScanThreads / kWarp];
   Opt<A> carry;
+  int first[kScanThreads / kWarp];  // look-back: nearest PREFIX per warp
+  Opt<C> lb[kScanThreads / kWarp];  // look-back: per-warp window folds
 };
+
+template <class S, class Op>
+using ScanSharedOf = ScanShared<typename ScanMath<S, Op>::A, typename ScanMath<S, Op>::C>;
 
 // Everything after the items are in registers: register scan, block scan,
 // publish + look-back, compose, store.  `raw` holds this thread's IT input
@@ -130,7 +135,7 @@ struct ScanShared {
 template <class T, class S, class F, class Op, bool Inclusive, int IT>
 __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, uint64_t tile,
                                                uint32_t epoch, const T (&raw)[IT], int count,
-                                               ScanShared<typename ScanMath<S, Op>::A>& sh) {
+                                               ScanSharedOf<S, Op>& sh) {
   using M = ScanMath<S, Op>;
   using A = typename M::A;
   using C = typename M::C;
@@ -180,13 +185,17 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
       sh.carry = cin;
       if (a.ntiles == 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
     }
-  } else if (warp == 0) {
+  } else {
+    // Block-wide look-back: every consumer thread polls one predecessor, so one
+    // L2 round trip inspects kScanThreads tiles.  (A single-warp window of 32
+    // caps the PREFIX frontier at ~32 tiles per round trip: ~1 TB/s of scan
+    // bandwidth at B200 latencies.)
     const C agg_c = M::to_c(agg.v);
-    if (lane == 0) IO::write(a.states, tile, epoch, kPartial, agg_c);
-    Opt<C> carry{C{}, false};
+    if (threadIdx.x == 0) IO::write(a.states, tile, epoch, kPartial, agg_c);
+    Opt<C> carry{C{}, false};  // meaningful in thread 0
     int64_t hi = int64_t(tile);
     for (;;) {
-      const int64_t j = hi - 1 - int64_t(lane);
+      const int64_t j = hi - 1 - int64_t(threadIdx.x);
       C val{};
       uint32_t kind = 0;
       if (j >= 0) {
@@ -194,21 +203,33 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
         }
       }
       const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
-      const int pl = pm ? __ffs(int(pm)) - 1 : kWarp - 1;
-      // Lanes 0..pl hold tiles hi-1 .. hi-1-pl (newest first): fold them with
-      // the older (higher) lane on the LEFT of every combine.
-      Opt<C> v{val, int(lane) <= pl && j >= 0};
+      if (lane == 0) sh.first[warp] = pm ? int(warp) * kWarp + __ffs(int(pm)) - 1 : kScanThreads;
+      consumer_sync();
+      int pl = kScanThreads;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
+      const bool found = pl < kScanThreads;
+      // Threads 0..pl hold tiles hi-1 .. hi-1-pl (newest first): fold them with
+      // the older (higher) thread on the LEFT of every combine.
+      Opt<C> v{val, int(threadIdx.x) <= pl && j >= 0};
 #pragma unroll
       for (unsigned d = 1; d < kWarp; d <<= 1) {
         Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
         if (lane + d < kWarp) v = opt_combine(cop, got, v);
       }
-      const Opt<C> window{shfl_idx(v.v, 0), __shfl_sync(kFullMask, int(v.has), 0) != 0};
-      carry = opt_combine(cop, window, carry);
-      if (pm) break;
-      hi -= kWarp;
+      if (lane == 0) sh.lb[warp] = v;
+      consumer_sync();
+      if (threadIdx.x == 0) {
+        Opt<C> window{C{}, false};
+#pragma unroll
+        for (int w = NW - 1; w >= 0; --w) window = opt_combine(cop, window, sh.lb[w]);
+        carry = opt_combine(cop, window, carry);
+      }
+      if (found) break;
+      hi -= kScanThreads;
+      consumer_sync();  // sh.first / sh.lb are rewritten by the next round
     }
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
       IO::write(a.states, tile, epoch, kPrefix, inclusive_c);
       sh.carry = Opt<A>{M::from_c(carry.v), true};
@@ -267,7 +288,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
   constexpr int IT = scan_items<S>();
   constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
   __shared__ uint32_t s_tile, s_epoch;
-  __shared__ ScanShared<A> sh;
+  __shared__ ScanSharedOf<S, Op> sh;
   if (threadIdx.x == 0) {
     // Epoch first, then the acq_rel claim: every CTA's epoch read happens
     // before the last claim, whose owner may then advance the epoch for the
@@ -350,7 +371,7 @@ __global__ void __launch_bounds__(kScanTmaThreads) scan_tma_kernel(const ScanArg
   __shared__ __align__(8) uint64_t empty[kScanStages];  // consumers done (count NW)
   __shared__ uint32_t ring[kScanStages];
   __shared__ uint32_t s_epoch;
-  __shared__ ScanShared<A> sh;
+  __shared__ ScanSharedOf<S, Op> sh;
 
   const bool tail_partial = (a.n % kTile) != 0;
   if (threadIdx.x == kScanThreads) {
@@ -443,6 +464,16 @@ inline uint32_t scan_tma_grid(uint64_t ntiles) {
   return uint32_t(ntiles < cap ? ntiles : cap);
 }
 
+// Kernel selection for contiguous aligned inputs: FORGE_SCAN_PATH=tma selects
+// the persistent TMA kernel, anything else the one-tile-per-CTA kernel.
+inline bool scan_use_tma() {
+  static const bool v = [] {
+    const char* e = std::getenv("FORGE_SCAN_PATH");
+    return e && std::strcmp(e, "tma") == 0;
+  }();
+  return v;
+}
+
 template <class T, class S, class F, class Op>
 cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_stride, uint64_t n,
                         bool inclusive, const F& f, const Op& op, const S& identity,
@@ -454,7 +485,8 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                           f,        op,        identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
                           static_cast<uint32_t*>(ws), uint32_t(ntiles)};
-  const bool tma = scan_tma_eligible<T, S>() && src_stride == 1 && is_aligned(src, 16) && ntiles >= 2;
+  const bool tma = scan_use_tma() && scan_tma_eligible<T, S>() && src_stride == 1 &&
+                   is_aligned(src, 16) && ntiles >= 2;
   if (tma) {
     const size_t smem = size_t(kScanStages) * scan_tile_bytes<T, S>();
     if (inclusive)

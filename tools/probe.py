@@ -1,0 +1,39 @@
+#!/usr/bin/env python3
+"""Quick kernel timing probe (development tool, not the bench contract).
+usage: python tools/probe.py scan|mapreduce|matrix [--check]"""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2603_18695_b200 import capi, dev
+from paper_2603_18695_b200.forge import op_info
+
+def t(fn, reps=10):
+    s = torch.cuda.current_stream(); fn(); torch.cuda.synchronize()
+    ev = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s); fn(); b.record(s); ev.append((a, b))
+    torch.cuda.synchronize()
+    x = sorted(a.elapsed_time(b) for a, b in ev); return x[len(x)//2]
+
+what = sys.argv[1] if len(sys.argv) > 1 else "scan"
+check = "--check" in sys.argv
+ws = dev.Workspace(); out = {}
+if what == "scan":
+    n = 1 << 28
+    for name, op, incl in (("f32_incl", capi.F32_SUM, True), ("i32_incl", capi.I32_SUM, True),
+                           ("affine", capi.AFFINE_F32, True), ("argmax", capi.ARGMAX_F32I32, True),
+                           ("mat2", capi.MAT2_U32, True)):
+        nn = n if op_info(op)["t_size"] <= 8 else n // 2
+        src = dev.empty(op, nn); dev.fill_synthetic(op, src, nn, 3); dst = dev.empty(op, nn, "S")
+        ms = t(lambda: dev.scan(op, incl, src, dst, nn, ws))
+        inf = op_info(op); gbs = nn * (inf["t_size"] + inf["s_size"]) / ms / 1e6
+        out[name] = round(gbs, 1)
+        if check:
+            from oracle import oracle as orc
+            import numpy as np
+            got = dst.cpu().numpy().view(orc.s_dtype(op))
+            bad, worst = orc.check_scan_synthetic(op, incl, nn, 3, got, 1e-5)
+            out[name + "_bad"] = bad
+        del src, dst
+print(json.dumps({"path": os.environ.get("FORGE_SCAN_PATH", "tile"), what: out}))
