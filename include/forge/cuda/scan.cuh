@@ -47,6 +47,7 @@ constexpr int kScanThreads = 256;
 constexpr int kScanStages = 3;
 constexpr uint32_t kPartial = 1, kPrefix = 2;
 constexpr uint32_t kNoTile = 0xffffffffu;
+constexpr int kLookbackPerThread = 4;  // look-back window = 256 * 4 predecessor tiles
 
 template <class C>
 struct TileStateIO {
@@ -186,32 +187,48 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
       if (a.ntiles == 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
     }
   } else {
-    // Block-wide look-back: every consumer thread polls one predecessor, so one
-    // L2 round trip inspects kScanThreads tiles.  (A single-warp window of 32
-    // caps the PREFIX frontier at ~32 tiles per round trip: ~1 TB/s of scan
-    // bandwidth at B200 latencies.)
+    // Block-wide look-back: each consumer thread polls kLookbackPerThread
+    // consecutive predecessors, so one L2 round trip inspects 1024 tiles — more
+    // than the tiles in flight on a B200 — and a tile finds a PREFIX in one
+    // round.  (A single-warp window of 32 caps the PREFIX frontier at ~32 tiles
+    // per round trip, ~1 TB/s at B200 latencies; measured in profiles/.)
+    constexpr int LB = kLookbackPerThread;
+    constexpr int WIN = kScanThreads * LB;
     const C agg_c = M::to_c(agg.v);
     if (threadIdx.x == 0) IO::write(a.states, tile, epoch, kPartial, agg_c);
     Opt<C> carry{C{}, false};  // meaningful in thread 0
     int64_t hi = int64_t(tile);
     for (;;) {
-      const int64_t j = hi - 1 - int64_t(threadIdx.x);
-      C val{};
-      uint32_t kind = 0;
-      if (j >= 0) {
-        while ((kind = IO::read(a.states, uint64_t(j), epoch, val)) == 0) {
+      C val[LB];
+      uint32_t kind[LB];
+      int first = WIN;
+#pragma unroll
+      for (int q = 0; q < LB; ++q) {
+        const int64_t j = hi - 1 - int64_t(threadIdx.x) * LB - q;
+        kind[q] = 0;
+        val[q] = C{};
+        if (j >= 0) {
+          while ((kind[q] = IO::read(a.states, uint64_t(j), epoch, val[q])) == 0) {
+          }
         }
+        if (kind[q] == kPrefix && first == WIN) first = int(threadIdx.x) * LB + q;
       }
-      const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
-      if (lane == 0) sh.first[warp] = pm ? int(warp) * kWarp + __ffs(int(pm)) - 1 : kScanThreads;
+      // nearest PREFIX over the block (position 0 = tile hi-1)
+      const unsigned pm = __ballot_sync(kFullMask, first < WIN);
+      const int wfirst = __shfl_sync(kFullMask, first, pm ? __ffs(int(pm)) - 1 : 0);
+      if (lane == 0) sh.first[warp] = pm ? wfirst : WIN;
       consumer_sync();
-      int pl = kScanThreads;
+      int pl = WIN;
 #pragma unroll
       for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
-      const bool found = pl < kScanThreads;
-      // Threads 0..pl hold tiles hi-1 .. hi-1-pl (newest first): fold them with
-      // the older (higher) thread on the LEFT of every combine.
-      Opt<C> v{val, int(threadIdx.x) <= pl && j >= 0};
+      const bool found = pl < WIN;
+      // Fold positions 0..pl, older (larger position) always on the LEFT.
+      Opt<C> v{C{}, false};
+#pragma unroll
+      for (int q = LB - 1; q >= 0; --q) {
+        const int pos = int(threadIdx.x) * LB + q;
+        if (kind[q] != 0 && pos <= pl) v = opt_combine(cop, v, Opt<C>{val[q], true});
+      }
 #pragma unroll
       for (unsigned d = 1; d < kWarp; d <<= 1) {
         Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
@@ -226,7 +243,7 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
         carry = opt_combine(cop, window, carry);
       }
       if (found) break;
-      hi -= kScanThreads;
+      hi -= WIN;
       consumer_sync();  // sh.first / sh.lb are rewritten by the next round
     }
     if (threadIdx.x == 0) {
