@@ -47,18 +47,22 @@ constexpr int kScanThreads = 256;
 constexpr int kScanStages = 3;
 constexpr uint32_t kPartial = 1, kPrefix = 2;
 constexpr uint32_t kNoTile = 0xffffffffu;
-constexpr int kLookbackPerThread = 4;  // look-back window = 256 * 4 predecessor tiles
+constexpr int kLookbackPerThread = 4;  // max look-back polls per thread (window 256 * 4)
+constexpr uint32_t kStateSlotWords = 32;  // 256-byte tile-state slots
 
 template <class C>
 struct TileStateIO {
   static constexpr int SW = Words<C>::N;  // 32-bit chunks of the carry
   static constexpr int STRIDE = SW <= 1 ? 1 : SW <= 2 ? 2 : SW <= 4 ? 4 : SW <= 8 ? 8 : 16;
 
-  static __device__ __forceinline__ void write(uint64_t* states, uint64_t tile, uint32_t epoch,
-                                               uint32_t kind, const C& v) {
+  // `stride` (64-bit words per tile, >= STRIDE) spreads tile states over L2
+  // slices: slices are selected at 256-byte granularity, and every CTA in
+  // flight polls the states of the most recent tiles.
+  static __device__ __forceinline__ void write(uint64_t* states, uint64_t tile, uint32_t stride,
+                                               uint32_t epoch, uint32_t kind, const C& v) {
     Words<C> w = to_words(v);
     const uint64_t hi = uint64_t((epoch << 2) | kind) << 32;
-    uint64_t* p = states + tile * STRIDE;
+    uint64_t* p = states + tile * stride;
     if constexpr (STRIDE == 1) {
       st_relaxed_gpu(p, hi | w.w[0]);
     } else {
@@ -73,8 +77,8 @@ struct TileStateIO {
 
   // Returns the kind (0 = not yet valid for this epoch) and the value.
   static __device__ __forceinline__ uint32_t read(const uint64_t* states, uint64_t tile,
-                                                  uint32_t epoch, C& v) {
-    const uint64_t* p = states + tile * STRIDE;
+                                                  uint32_t stride, uint32_t epoch, C& v) {
+    const uint64_t* p = states + tile * stride;
     uint64_t raw[STRIDE];
     if constexpr (STRIDE == 1) {
       raw[0] = ld_relaxed_gpu(p);
@@ -108,8 +112,10 @@ struct ScanArgs {
   const S* carry_in;  // nullable, device
   S* total_out;       // nullable, device
   uint64_t* states;   // [ntiles * STRIDE] 64-bit words
-  uint32_t* ctrl;     // [0] ticket, [1] done counter, [2] epoch
+  uint32_t* ctrl;     // [0] ticket, [2] epoch
   uint32_t ntiles;
+  uint32_t state_stride;  // 64-bit words per tile state
+  uint32_t lookback;      // look-back polls per consumer thread (0 = warp 0 only, window 32)
 };
 
 // The 256 consumer threads synchronise on named barrier 1, so a producer warp
@@ -182,7 +188,7 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
         cin = Opt<A>{M::lift(*a.carry_in), true};
         pre = cop(M::to_c(cin.v), pre);
       }
-      IO::write(a.states, 0, epoch, kPrefix, pre);
+      IO::write(a.states, 0, a.state_stride, epoch, kPrefix, pre);
       sh.carry = cin;
       if (a.ntiles == 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
     }
@@ -193,62 +199,91 @@ __device__ __forceinline__ void scan_tile_body(const ScanArgs<T, S, F, Op>& a, u
     // round.  (A single-warp window of 32 caps the PREFIX frontier at ~32 tiles
     // per round trip, ~1 TB/s at B200 latencies; measured in profiles/.)
     constexpr int LB = kLookbackPerThread;
-    constexpr int WIN = kScanThreads * LB;
     const C agg_c = M::to_c(agg.v);
-    if (threadIdx.x == 0) IO::write(a.states, tile, epoch, kPartial, agg_c);
+    if (threadIdx.x == 0) IO::write(a.states, tile, a.state_stride, epoch, kPartial, agg_c);
     Opt<C> carry{C{}, false};  // meaningful in thread 0
-    int64_t hi = int64_t(tile);
-    for (;;) {
-      C val[LB];
-      uint32_t kind[LB];
-      int first = WIN;
-#pragma unroll
-      for (int q = 0; q < LB; ++q) {
-        const int64_t j = hi - 1 - int64_t(threadIdx.x) * LB - q;
-        kind[q] = 0;
-        val[q] = C{};
-        if (j >= 0) {
-          while ((kind[q] = IO::read(a.states, uint64_t(j), epoch, val[q])) == 0) {
+    if (a.lookback == 0) {
+      // Warp 0 alone: lanes poll the 32 nearest predecessors per round.
+      if (warp == 0) {
+        int64_t hi = int64_t(tile);
+        for (;;) {
+          const int64_t j = hi - 1 - int64_t(lane);
+          C val{};
+          uint32_t kind = 0;
+          if (j >= 0) {
+            while ((kind = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val)) == 0) {
+            }
           }
+          const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
+          const int pl = pm ? __ffs(int(pm)) - 1 : kWarp - 1;
+          Opt<C> v{val, int(lane) <= pl && j >= 0};
+#pragma unroll
+          for (unsigned d = 1; d < kWarp; d <<= 1) {
+            Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
+            if (lane + d < kWarp) v = opt_combine(cop, got, v);
+          }
+          const Opt<C> window{shfl_idx(v.v, 0), __shfl_sync(kFullMask, int(v.has), 0) != 0};
+          carry = opt_combine(cop, window, carry);
+          if (pm) break;
+          hi -= kWarp;
         }
-        if (kind[q] == kPrefix && first == WIN) first = int(threadIdx.x) * LB + q;
       }
-      // nearest PREFIX over the block (position 0 = tile hi-1)
-      const unsigned pm = __ballot_sync(kFullMask, first < WIN);
-      const int wfirst = __shfl_sync(kFullMask, first, pm ? __ffs(int(pm)) - 1 : 0);
-      if (lane == 0) sh.first[warp] = pm ? wfirst : WIN;
-      consumer_sync();
-      int pl = WIN;
+    } else {
+      const int lbn = int(a.lookback < uint32_t(LB) ? a.lookback : uint32_t(LB));
+      const int WIN = kScanThreads * lbn;
+      int64_t hi = int64_t(tile);
+      for (;;) {
+        C val[LB];
+        uint32_t kind[LB];
+        int first = WIN;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
-      const bool found = pl < WIN;
-      // Fold positions 0..pl, older (larger position) always on the LEFT.
-      Opt<C> v{C{}, false};
+        for (int q = 0; q < LB; ++q) {
+          kind[q] = 0;
+          val[q] = C{};
+          const int64_t j = hi - 1 - int64_t(threadIdx.x) * lbn - q;
+          if (q < lbn && j >= 0) {
+            while ((kind[q] = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val[q])) == 0) {
+            }
+          }
+          if (kind[q] == kPrefix && first == WIN) first = int(threadIdx.x) * lbn + q;
+        }
+        // nearest PREFIX over the block (position 0 = tile hi-1)
+        const unsigned pm = __ballot_sync(kFullMask, first < WIN);
+        const int wfirst = __shfl_sync(kFullMask, first, pm ? __ffs(int(pm)) - 1 : 0);
+        if (lane == 0) sh.first[warp] = pm ? wfirst : WIN;
+        consumer_sync();
+        int pl = WIN;
 #pragma unroll
-      for (int q = LB - 1; q >= 0; --q) {
-        const int pos = int(threadIdx.x) * LB + q;
-        if (kind[q] != 0 && pos <= pl) v = opt_combine(cop, v, Opt<C>{val[q], true});
+        for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
+        const bool found = pl < WIN;
+        // Fold positions 0..pl, older (larger position) always on the LEFT.
+        Opt<C> v{C{}, false};
+#pragma unroll
+        for (int q = LB - 1; q >= 0; --q) {
+          const int pos = int(threadIdx.x) * lbn + q;
+          if (kind[q] != 0 && pos <= pl) v = opt_combine(cop, v, Opt<C>{val[q], true});
+        }
+#pragma unroll
+        for (unsigned d = 1; d < kWarp; d <<= 1) {
+          Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
+          if (lane + d < kWarp) v = opt_combine(cop, got, v);
+        }
+        if (lane == 0) sh.lb[warp] = v;
+        consumer_sync();
+        if (threadIdx.x == 0) {
+          Opt<C> window{C{}, false};
+#pragma unroll
+          for (int w = NW - 1; w >= 0; --w) window = opt_combine(cop, window, sh.lb[w]);
+          carry = opt_combine(cop, window, carry);
+        }
+        if (found) break;
+        hi -= WIN;
+        consumer_sync();  // sh.first / sh.lb are rewritten by the next round
       }
-#pragma unroll
-      for (unsigned d = 1; d < kWarp; d <<= 1) {
-        Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
-        if (lane + d < kWarp) v = opt_combine(cop, got, v);
-      }
-      if (lane == 0) sh.lb[warp] = v;
-      consumer_sync();
-      if (threadIdx.x == 0) {
-        Opt<C> window{C{}, false};
-#pragma unroll
-        for (int w = NW - 1; w >= 0; --w) window = opt_combine(cop, window, sh.lb[w]);
-        carry = opt_combine(cop, window, carry);
-      }
-      if (found) break;
-      hi -= WIN;
-      consumer_sync();  // sh.first / sh.lb are rewritten by the next round
     }
     if (threadIdx.x == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
-      IO::write(a.states, tile, epoch, kPrefix, inclusive_c);
+      IO::write(a.states, tile, a.state_stride, epoch, kPrefix, inclusive_c);
       sh.carry = Opt<A>{M::from_c(carry.v), true};
       if (tile == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(inclusive_c);
     }
@@ -458,9 +493,11 @@ struct ScanWs {
   using C = typename CarryTraits<S, Op>::C;
   static constexpr uint64_t kTile = uint64_t(kScanThreads) * scan_items<S>();
   static uint64_t tiles(uint64_t n) { return ceil_div(n, kTile); }
-  static uint64_t bytes(uint64_t n) {
-    return 256 + tiles(n) * TileStateIO<C>::STRIDE * sizeof(uint64_t);
-  }
+  // Each tile state owns a 256-byte slot (one L2-slice granule); larger
+  // carries (> 256 B) take their natural size.
+  static constexpr uint32_t kSlotWords =
+      TileStateIO<C>::STRIDE > kStateSlotWords ? TileStateIO<C>::STRIDE : kStateSlotWords;
+  static uint64_t bytes(uint64_t n) { return 256 + tiles(n) * kSlotWords * sizeof(uint64_t); }
 };
 
 template <class T, class S, class F, class Op, bool Inclusive>
@@ -491,6 +528,22 @@ inline bool scan_use_tma() {
   return v;
 }
 
+// Experiment knobs (defaults are the tuned values): FORGE_SCAN_LOOKBACK = polls
+// per thread of the block-wide look-back (0 = warp 0 only, window 32);
+// FORGE_SCAN_STATE_WORDS = 64-bit words between consecutive tile states.
+inline uint32_t scan_env_u32(const char* name, uint32_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? uint32_t(std::strtoul(e, nullptr, 10)) : dflt;
+}
+inline uint32_t scan_lookback_mode() {
+  static const uint32_t v = scan_env_u32("FORGE_SCAN_LOOKBACK", 0);
+  return v;
+}
+inline uint32_t scan_state_words_override() {
+  static const uint32_t v = scan_env_u32("FORGE_SCAN_STATE_WORDS", 0);
+  return v;
+}
+
 template <class T, class S, class F, class Op>
 cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_stride, uint64_t n,
                         bool inclusive, const F& f, const Op& op, const S& identity,
@@ -501,7 +554,12 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   ScanArgs<T, S, F, Op> a{src,      dst,       n,         src_stride, dst_stride,
                           f,        op,        identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
-                          static_cast<uint32_t*>(ws), uint32_t(ntiles)};
+                          static_cast<uint32_t*>(ws), uint32_t(ntiles),
+                          ScanWs<T, S, Op>::kSlotWords, scan_lookback_mode()};
+  {
+    const uint32_t w = scan_state_words_override();
+    if (w >= TileStateIO<typename CarryTraits<S, Op>::C>::STRIDE && w <= a.state_stride) a.state_stride = w;
+  }
   const bool tma = scan_use_tma() && scan_tma_eligible<T, S>() && src_stride == 1 &&
                    is_aligned(src, 16) && ntiles >= 2;
   if (tma) {

@@ -203,7 +203,7 @@ inline uint64_t b200_state_bytes(uint32_t accum_size) {
   const uint64_t words = (2ull * accum_size + 3) / 4;
   uint64_t stride = 1;
   while (stride < words) stride <<= 1;
-  return stride * 8;
+  return std::max<uint64_t>(stride * 8, 256);  // 256-byte slot per tile (cuda::kStateSlotWords)
 }
 inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
   const uint64_t tiles = (n + b200_scan_tile(accum_size) - 1) / b200_scan_tile(accum_size);

@@ -75,8 +75,8 @@ def test_arch_params_defaults_and_workspace_sizing():
     p = F.ArchParams()
     assert (p.warp_width, p.mapreduce_blocks, p.threads_per_block, p.nitem_scan) == (32, 100, 256, 16)
     # B200 workspace sizes: scan tile = 4096 f32 -> 1 tile state (16 B with the f64 carry) + control
-    assert F.required_workspace(capi.PRIM_SCAN, 4, 4096) == 256 + 16
-    assert F.required_workspace(capi.PRIM_SCAN, 4, 4097) == 256 + 32
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 4096) == 256 + 256
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 4097) == 256 + 512
     assert F.required_workspace(capi.PRIM_VCOPY, 4, 100) == 0
     with pytest.raises(F.ForgeError) as e:
         F.required_workspace(capi.PRIM_SCAN, 4, 10, params=F.ArchParams(warp_width=64, threads_per_block=256))
