@@ -117,7 +117,20 @@ struct ScanArgs {
   uint32_t ntiles;
   uint32_t state_stride;  // 64-bit words per tile state slot
   uint32_t lookback;      // 0: warp 0 polls 32 predecessors; k: 256*k predecessors block-wide
+  uint64_t* trace;        // optional per-tile phase timestamps (FORGE_SCAN_TRACE), else null
 };
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Phase timestamps of a tile: 0 claimed, 1 data landed, 2 pass 1 done,
+// 3 prefix known (look-back done), 4 pass 2 done; 5 = SM id.
+__device__ __forceinline__ void trace_mark(uint64_t* trace, uint64_t tile, int phase) {
+  if (trace && threadIdx.x == 0) trace[tile * 8 + phase] = global_ns();
+}
 
 template <class A, class C>
 struct ScanShared {
@@ -406,6 +419,12 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   __syncthreads();
   const uint64_t tile = s_tile;
+  trace_mark(a.trace, tile, 0);
+  if (a.trace && threadIdx.x == 0) {
+    uint32_t sm;
+    asm("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.trace[tile * 8 + 5] = sm;
+  }
   const bool full = (tile + 1) * kTile <= a.n;
   const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * IT;
   const uint64_t avail = base < a.n ? a.n - base : 0;
@@ -415,6 +434,7 @@ __global__ void __launch_bounds__(kScanThreads)
   Opt<A> tot{A{}, false};
   if (full) {
     mbar_wait(&bar, 0);
+    trace_mark(a.trace, tile, 1);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
       const uint4 v = lds128(tile_mem + swz128(threadIdx.x, c));
@@ -435,7 +455,9 @@ __global__ void __launch_bounds__(kScanThreads)
     tot.has = count > 0;
   }
 
+  trace_mark(a.trace, tile, 2);
   Opt<A> run = block_exclusive_prefix(a, tile, s_epoch, tot, sh);
+  trace_mark(a.trace, tile, 3);
   if (count == 0) return;
 
   // ---- pass 2: running prefixes, stored as they are produced
@@ -468,6 +490,7 @@ __global__ void __launch_bounds__(kScanThreads)
         for (int e = 0; e < EPC; ++e) d[e] = o[e];
       }
     }
+    trace_mark(a.trace, tile, 4);
   } else {
     for (int k = 0; k < count; ++k) {
       const A y = M::lift(a.f(a.src[base + k]));
@@ -547,7 +570,9 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   ScanArgs<T, S, F, Op> a{src,      dst,      n,         src_stride, dst_stride,
                           f,        op,       identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
-                          static_cast<uint32_t*>(ws), 0u, WsT::kSlotWords, scan_lookback_mode()};
+                          static_cast<uint32_t*>(ws), 0u, WsT::kSlotWords, scan_lookback_mode(), nullptr};
+  if (scan_env_u32("FORGE_SCAN_TRACE", 0))  // development: phase timestamps after the tile states
+    a.trace = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + WsT::bytes(n));
   {
     const uint32_t w = scan_state_words_override();
     if (w >= TileStateIO<typename CarryTraits<S, Op>::C>::STRIDE && w <= a.state_stride) a.state_stride = w;
