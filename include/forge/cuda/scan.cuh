@@ -206,13 +206,22 @@ __device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> block_exclusive_pref
     if (a.lookback == 0) {
       if (warp == 0) {
         int64_t hi = int64_t(tile);
+        uint32_t windows = 0, polls = 0;
         for (;;) {
+          ++windows;
           const int64_t j = hi - 1 - int64_t(lane);
           C val{};
           uint32_t kind = 0;
           if (j >= 0) {
             while ((kind = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val)) == 0) {
+              if (a.trace) ++polls;
             }
+          }
+          if (a.trace && lane == 0) {
+            a.trace[tile * 8 + 6] = windows;
+            a.trace[tile * 8 + 7] = __reduce_max_sync(kFullMask, polls) + windows;
+          } else if (a.trace) {
+            __reduce_max_sync(kFullMask, polls);
           }
           const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
           const int pl = pm ? __ffs(int(pm)) - 1 : kWarp - 1;
