@@ -397,9 +397,13 @@ constexpr int smem_scan_items() {
 constexpr uint32_t kSmemTileBytes = uint32_t(kScanThreads) * kRowBytes;  // 32 KB
 constexpr uint32_t kSmemScanDyn = kSmemTileBytes + 1024;                 // + swizzle alignment slack
 
+// `tmap_out` (used when tma_store) views dst as 128-byte rows; only for
+// sizeof(S) == sizeof(T), where each output chunk overwrites its input chunk
+// in shared memory and the finished tile leaves with one TMA tensor store.
 template <class T, class S, class F, class Op, bool Inclusive>
 __global__ void __launch_bounds__(kScanThreads)
-    scan_smem_kernel(const ScanArgs<T, S, F, Op> a, const __grid_constant__ CUtensorMap tmap) {
+    scan_smem_kernel(const ScanArgs<T, S, F, Op> a, const __grid_constant__ CUtensorMap tmap,
+                     const __grid_constant__ CUtensorMap tmap_out, bool tma_store) {
   using M = ScanMath<S, Op>;
   using A = typename M::A;
   constexpr int IT = smem_scan_items<T>();  // items per thread (one 128-byte row)
@@ -408,22 +412,36 @@ __global__ void __launch_bounds__(kScanThreads)
   constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
   extern __shared__ unsigned char dyn_smem[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t s_tile, s_epoch;
+  __shared__ uint32_t s_tile, s_epoch, s_phase;
   __shared__ ScanSharedOf<S, Op> sh;
   auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
   unsigned char* tile_mem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
 
   if (threadIdx.x == 0) {
+    // The tile to load is guessed as blockIdx.x and its TMA issued BEFORE the
+    // ticket round trip (CTAs are dispatched in index order in practice); the
+    // ticket stays the source of truth, so a mismatch only costs a reload.
+    const uint32_t g = blockIdx.x;
+    const bool gfull = uint64_t(g + 1) * kTile <= a.n;
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    if (gfull) {
+      mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+      tma_load_2d(tile_mem, &tmap, 0, int(g) * kScanThreads, &bar);
+    }
     uint32_t e;
     const uint32_t t = claim_tile(a, e);
     s_tile = t;
     s_epoch = e;
-    if (uint64_t(t + 1) * kTile <= a.n) {
-      mbar_init(&bar, 1);
-      fence_mbar_init();
-      mbar_arrive_expect_tx(&bar, kSmemTileBytes);
-      tma_load_2d(tile_mem, &tmap, 0, int(t) * kScanThreads, &bar);
+    s_phase = 0;
+    if (t != g) {
+      if (gfull) mbar_wait(&bar, 0);  // drain the speculative copy
+      if (uint64_t(t + 1) * kTile <= a.n) {
+        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+        tma_load_2d(tile_mem, &tmap, 0, int(t) * kScanThreads, &bar);
+        s_phase = gfull ? 1u : 0u;
+      }
     }
   }
   __syncthreads();
@@ -442,7 +460,7 @@ __global__ void __launch_bounds__(kScanThreads)
   // ---- pass 1: ordered fold of this thread's row
   Opt<A> tot{A{}, false};
   if (full) {
-    mbar_wait(&bar, 0);
+    mbar_wait(&bar, s_phase);
     trace_mark(a.trace, tile, 1);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -491,12 +509,31 @@ __global__ void __launch_bounds__(kScanThreads)
           run.has = true;
         }
       }
+      if constexpr (sizeof(S) == sizeof(T)) {
+        if (tma_store) {
+          uint4 w;
+          memcpy(&w, o, 16);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(tile_mem + swz128(threadIdx.x, c))),
+                       "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                       : "memory");
+          continue;
+        }
+      }
       S* d = a.dst + base + uint64_t(c) * EPC;
       if (vec) {
         store_items<S, EPC>(d, o);
       } else {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) d[e] = o[e];
+      }
+    }
+    if (sizeof(S) == sizeof(T) && tma_store) {
+      fence_proxy_async_smem();  // generic smem writes -> visible to the TMA engine
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_store_2d(&tmap_out, 0, int(tile) * kScanThreads, tile_mem);
+        tma_store_commit();
+        tma_store_wait_read();  // keep the CTA (and its smem) alive until read
       }
     }
     trace_mark(a.trace, tile, 4);
@@ -592,12 +629,15 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                     make_rows128_map(&tmap, src, (n * sizeof(T)) / kRowBytes, uint32_t(kScanThreads));
   if (smem) {
     a.ntiles = uint32_t(ceil_div(n, WsT::kTileSmem));
+    CUtensorMap tmap_out = tmap;
+    const bool tstore = sizeof(S) == sizeof(T) && !scan_env_u32("FORGE_SCAN_NO_TMA_STORE", 0) &&
+                        make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
     if (inclusive) {
       scan_smem_prepare<T, S, F, Op, true>();
-      scan_smem_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap);
+      scan_smem_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap, tmap_out, tstore);
     } else {
       scan_smem_prepare<T, S, F, Op, false>();
-      scan_smem_kernel<T, S, F, Op, false><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap);
+      scan_smem_kernel<T, S, F, Op, false><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap, tmap_out, tstore);
     }
   } else {
     a.ntiles = uint32_t(ceil_div(n, WsT::kTileGeneral));
