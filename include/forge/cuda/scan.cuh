@@ -602,6 +602,11 @@ inline void scan_smem_prepare() {
   if (done_dev != dev) {
     cudaFuncSetAttribute(scan_smem_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kSmemScanDyn));
+    // Maximum shared-memory carveout: residency (tiles in flight) is what
+    // hides the look-back latency; the kernel barely uses L1.
+    cudaFuncSetAttribute(scan_smem_kernel<T, S, F, Op, Inclusive>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout,
+                         int(scan_env_u32("FORGE_SCAN_CARVEOUT", 100)));
     done_dev = dev;
   }
 }
