@@ -554,6 +554,357 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 // ---------------------------------------------------------------------------
+// Fast path v3: persistent, software-pipelined tiles.
+//
+// Measured on the one-tile-per-CTA kernel (profiles/): a tile lives ~8 us, of
+// which ~5.4 us is the look-back, spent waiting for the most recent
+// predecessors' PARTIALs — whose publication is gated by their own TMA
+// landing-time tail (head-of-line blocking).  Here a producer warp claims
+// tickets and keeps kPipeStages tiles in flight with 2-D TMA; the 256 consumer
+// threads run, per iteration,
+//     A(next tile): fold rows from smem, block scan, publish PARTIAL
+//     look-back(current tile) -> PREFIX        (its predecessors' PARTIALs were
+//                                                published an iteration earlier)
+//     C(current tile): running prefixes written back into the smem tile,
+//                      one TMA tensor store, stage released to the producer.
+// Deadlock-freedom without co-residency: tiles are claimed in ticket order and
+// each CTA processes its claims in order, so the owner of the smallest
+// unfinished tile is always at that tile's A or look-back, which waits only on
+// smaller (finished) tiles.
+
+constexpr int kPipeStages = 3;
+constexpr int kPipeThreads = kScanThreads + kWarp;  // + 1 producer warp
+constexpr uint32_t kPipeDyn = kPipeStages * kSmemTileBytes + 1024;
+constexpr uint32_t kNoTile = 0xffffffffu;
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kScanThreads) : "memory");
+}
+
+template <class A, class C>
+struct PipeShared {
+  Opt<A> warp[kScanThreads / kWarp];
+  Opt<A> carry;
+  int first[kScanThreads / kWarp];
+  Opt<C> lb[kScanThreads / kWarp];
+};
+
+template <class S, class Op>
+using PipeSharedOf = PipeShared<typename ScanMath<S, Op>::A, typename ScanMath<S, Op>::C>;
+
+// Block scan of the 256 row totals: returns the row's exclusive prefix WITHIN
+// the tile; `agg` receives the tile aggregate (all threads).
+template <class A, class Sh, class AOp>
+__device__ __forceinline__ Opt<A> pipe_tile_scan(const AOp& aop, const Opt<A>& tot, Sh& sh, Opt<A>& agg) {
+  constexpr int NW = kScanThreads / kWarp;
+  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
+  const Opt<A> incl = warp_scan_incl(aop, tot);
+  if (lane == kWarp - 1) sh.warp[warp] = incl;
+  consumer_sync();
+  if (warp == 0) {
+    Opt<A> w = lane < NW ? sh.warp[lane] : Opt<A>{A{}, false};
+    w = warp_scan_incl(aop, w);
+    if (lane < NW) sh.warp[lane] = w;
+  }
+  consumer_sync();
+  agg = sh.warp[NW - 1];
+  const Opt<A> warp_ex = warp > 0 ? sh.warp[warp - 1] : Opt<A>{A{}, false};
+  Opt<A> lane_ex = shfl_up_opt(incl, 1);
+  if (lane == 0) lane_ex.has = false;
+  const Opt<A> ex = opt_combine(aop, warp_ex, lane_ex);
+  consumer_sync();  // sh.warp is reused by the next tile
+  return ex;
+}
+
+// Block-wide look-back for tile > 0 whose aggregate is already PARTIAL.
+// Publishes PREFIX; returns the tile's exclusive carry to every consumer thread.
+template <class T, class S, class F, class Op>
+__device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> pipe_lookback(
+    const ScanArgs<T, S, F, Op>& a, uint64_t tile, uint32_t epoch, const typename ScanMath<S, Op>::C& agg_c,
+    PipeSharedOf<S, Op>& sh) {
+  using M = ScanMath<S, Op>;
+  using A = typename M::A;
+  using C = typename M::C;
+  using IO = TileStateIO<C>;
+  constexpr int NW = kScanThreads / kWarp;
+  constexpr int LB = kLookbackPerThread;
+  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
+  auto cop = [&](const C& x, const C& y) { return M::CT::op(a.op, x, y); };
+  const int lbn = int(a.lookback == 0 ? 1u : (a.lookback < uint32_t(LB) ? a.lookback : uint32_t(LB)));
+  const int WIN = kScanThreads * lbn;
+  Opt<C> carry{C{}, false};  // meaningful in thread 0
+  int64_t hi = int64_t(tile);
+  for (;;) {
+    C val[LB];
+    uint32_t kind[LB];
+    int first = WIN;
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      kind[q] = 0;
+      val[q] = C{};
+      const int64_t j = hi - 1 - int64_t(threadIdx.x) * lbn - q;
+      if (q < lbn && j >= 0) {
+        while ((kind[q] = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val[q])) == 0) {
+        }
+      }
+      if (kind[q] == kPrefix && first == WIN) first = int(threadIdx.x) * lbn + q;
+    }
+    const unsigned pm = __ballot_sync(kFullMask, first < WIN);
+    const int wfirst = __shfl_sync(kFullMask, first, pm ? __ffs(int(pm)) - 1 : 0);
+    if (lane == 0) sh.first[warp] = pm ? wfirst : WIN;
+    consumer_sync();
+    int pl = WIN;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
+    const bool found = pl < WIN;
+    // Fold positions 0..pl (position 0 = tile hi-1), older always on the LEFT.
+    Opt<C> v{C{}, false};
+#pragma unroll
+    for (int q = LB - 1; q >= 0; --q) {
+      const int pos = int(threadIdx.x) * lbn + q;
+      if (kind[q] != 0 && pos <= pl) v = opt_combine(cop, v, Opt<C>{val[q], true});
+    }
+#pragma unroll
+    for (unsigned d = 1; d < kWarp; d <<= 1) {
+      Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
+      if (lane + d < kWarp) v = opt_combine(cop, got, v);
+    }
+    if (lane == 0) sh.lb[warp] = v;
+    consumer_sync();
+    if (threadIdx.x == 0) {
+      Opt<C> window{C{}, false};
+#pragma unroll
+      for (int w = NW - 1; w >= 0; --w) window = opt_combine(cop, window, sh.lb[w]);
+      carry = opt_combine(cop, window, carry);
+    }
+    consumer_sync();  // sh.first / sh.lb reuse
+    if (found) break;
+    hi -= WIN;
+  }
+  if (threadIdx.x == 0) {
+    const C inclusive_c = cop(carry.v, agg_c);
+    IO::write(a.states, tile, a.state_stride, epoch, kPrefix, inclusive_c);
+    sh.carry = Opt<A>{M::from_c(carry.v), true};
+    if (tile == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(inclusive_c);
+  }
+  consumer_sync();
+  const Opt<A> r = sh.carry;
+  consumer_sync();
+  return r;
+}
+
+template <class T, class S, class F, class Op, bool Inclusive>
+__global__ void __launch_bounds__(kPipeThreads)
+    scan_pipe_kernel(const ScanArgs<T, S, F, Op> a, const __grid_constant__ CUtensorMap tmap,
+                     const __grid_constant__ CUtensorMap tmap_out, bool tma_store) {
+  using M = ScanMath<S, Op>;
+  using A = typename M::A;
+  using C = typename M::C;
+  using IO = TileStateIO<C>;
+  constexpr int IT = smem_scan_items<T>();
+  constexpr int EPC = 16 / int(sizeof(T));
+  constexpr int NCH = kRowBytes / 16;
+  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
+  extern __shared__ unsigned char dyn_smem[];
+  __shared__ __align__(8) uint64_t full[kPipeStages];
+  __shared__ __align__(8) uint64_t empty[kPipeStages];
+  __shared__ uint32_t ring[kPipeStages];
+  __shared__ uint32_t s_epoch;
+  __shared__ PipeSharedOf<S, Op> sh;
+  auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
+  unsigned char* stage_mem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
+  const bool tail_partial = (a.n % kTile) != 0;
+
+  if (threadIdx.x == kScanThreads) {
+    for (int s = 0; s < kPipeStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (threadIdx.x >= kScanThreads) {
+    // ---- producer: epoch first, then tickets (acq_rel) in order, each CTA
+    // until its first failure -> exactly ntiles + gridDim.x claims per launch.
+    if (threadIdx.x != kScanThreads) return;
+    const uint32_t epoch = ld_acquire_gpu(a.ctrl + 2);
+    s_epoch = epoch;
+    for (uint32_t it = 0;; ++it) {
+      const int s = int(it % kPipeStages);
+      if (it >= uint32_t(kPipeStages)) mbar_wait(&empty[s], ((it / kPipeStages) - 1) & 1u);
+      uint32_t t = atom_add_acq_rel_gpu(a.ctrl + 0, 1u);
+      if (t == a.ntiles + gridDim.x - 1) {
+        st_relaxed_gpu(a.ctrl + 0, 0u);
+        st_relaxed_gpu(a.ctrl + 2, epoch + 1u);
+      }
+      if (t >= a.ntiles) t = kNoTile;
+      ring[s] = t;
+      if (t != kNoTile && !(tail_partial && t == a.ntiles - 1)) {
+        mbar_arrive_expect_tx(&full[s], kSmemTileBytes);
+        tma_load_2d(stage_mem + size_t(s) * kSmemTileBytes, &tmap, 0, int(t) * kScanThreads, &full[s]);
+      } else {
+        mbar_arrive(&full[s]);  // end marker, or the partial last tile (read from global)
+      }
+      if (t == kNoTile) return;
+    }
+  }
+
+  // ---- consumers
+  // A(tile): fold the rows, block scan, publish; returns the row's in-tile exclusive prefix.
+  auto phase_a = [&](uint32_t tile, int s, uint32_t epoch, C& agg_c) -> Opt<A> {
+    const bool fulltile = !(tail_partial && tile == a.ntiles - 1);
+    const uint64_t base = uint64_t(tile) * kTile + uint64_t(threadIdx.x) * IT;
+    const unsigned char* tm = stage_mem + size_t(s) * kSmemTileBytes;
+    Opt<A> tot{A{}, false};
+    if (fulltile) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint4 v = lds128(tm + swz128(threadIdx.x, c));
+        T x[EPC];
+        memcpy(x, &v, 16);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const A y = M::lift(a.f(x[e]));
+          tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
+        }
+      }
+      tot.has = true;
+    } else {
+      const uint64_t avail = base < a.n ? a.n - base : 0;
+      const int cnt = avail >= uint64_t(IT) ? IT : int(avail);
+      for (int k = 0; k < cnt; ++k) {
+        const A y = M::lift(a.f(a.src[base + k]));
+        tot.v = k == 0 ? y : aop(tot.v, y);
+      }
+      tot.has = cnt > 0;
+    }
+    Opt<A> agg;
+    const Opt<A> ex = pipe_tile_scan(aop, tot, sh, agg);
+    agg_c = M::to_c(agg.v);
+    if (threadIdx.x == 0) {
+      if (tile == 0) {
+        C pre = agg_c;
+        if (a.carry_in) pre = M::CT::op(a.op, M::to_c(M::lift(*a.carry_in)), pre);
+        IO::write(a.states, 0, a.state_stride, epoch, kPrefix, pre);
+        if (a.ntiles == 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
+      } else {
+        IO::write(a.states, tile, a.state_stride, epoch, kPartial, agg_c);
+      }
+    }
+    return ex;
+  };
+
+  // C(tile): running prefixes from `run` (the row's exclusive prefix).
+  auto phase_c = [&](uint32_t tile, int s, Opt<A> run) {
+    const bool fulltile = !(tail_partial && tile == a.ntiles - 1);
+    const uint64_t base = uint64_t(tile) * kTile + uint64_t(threadIdx.x) * IT;
+    unsigned char* tm = stage_mem + size_t(s) * kSmemTileBytes;
+    if (fulltile) {
+      const bool vec = is_aligned(a.dst + base, 16);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint4 v = lds128(tm + swz128(threadIdx.x, c));
+        T x[EPC];
+        memcpy(x, &v, 16);
+        S o[EPC];
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const A y = M::lift(a.f(x[e]));
+          if constexpr (Inclusive) {
+            run.v = run.has ? aop(run.v, y) : y;
+            run.has = true;
+            o[e] = M::lower(run.v);
+          } else {
+            o[e] = run.has ? M::lower(run.v) : a.identity;
+            run.v = run.has ? aop(run.v, y) : y;
+            run.has = true;
+          }
+        }
+        if constexpr (sizeof(S) == sizeof(T)) {
+          if (tma_store) {
+            uint4 w;
+            memcpy(&w, o, 16);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(tm + swz128(threadIdx.x, c))),
+                         "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                         : "memory");
+            continue;
+          }
+        }
+        S* d = a.dst + base + uint64_t(c) * EPC;
+        if (vec) {
+          store_items<S, EPC>(d, o);
+        } else {
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) d[e] = o[e];
+        }
+      }
+      if (sizeof(S) == sizeof(T) && tma_store) {
+        fence_proxy_async_smem();
+        consumer_sync();
+        if (threadIdx.x == 0) {
+          tma_store_2d(&tmap_out, 0, int(tile) * kScanThreads, tm);
+          tma_store_commit();
+          tma_store_wait_read();
+        }
+      } else {
+        consumer_sync();
+      }
+    } else {
+      const uint64_t avail = base < a.n ? a.n - base : 0;
+      const int cnt = avail >= uint64_t(IT) ? IT : int(avail);
+      for (int k = 0; k < cnt; ++k) {
+        const A y = M::lift(a.f(a.src[base + k]));
+        if constexpr (Inclusive) {
+          run.v = run.has ? aop(run.v, y) : y;
+          run.has = true;
+          a.dst[base + k] = M::lower(run.v);
+        } else {
+          a.dst[base + k] = run.has ? M::lower(run.v) : a.identity;
+          run.v = run.has ? aop(run.v, y) : y;
+          run.has = true;
+        }
+      }
+      consumer_sync();
+    }
+    if (threadIdx.x == 0) mbar_arrive(&empty[s]);  // stage free for the producer
+  };
+
+  uint32_t it = 0;
+  int s_cur = 0;
+  mbar_wait(&full[0], 0);
+  uint32_t cur = ring[0];
+  if (cur == kNoTile) return;
+  const uint32_t epoch = s_epoch;
+  C agg_cur;
+  Opt<A> ex_cur = phase_a(cur, 0, epoch, agg_cur);
+  for (;;) {
+    const uint32_t it_next = it + 1;
+    const int s_next = int(it_next % kPipeStages);
+    mbar_wait(&full[s_next], (it_next / kPipeStages) & 1u);
+    const uint32_t nxt = ring[s_next];
+    C agg_next{};
+    Opt<A> ex_next{A{}, false};
+    if (nxt != kNoTile) ex_next = phase_a(nxt, s_next, epoch, agg_next);
+    // look-back of the current tile
+    Opt<A> carry{A{}, false};
+    if (cur == 0) {
+      if (a.carry_in) carry = Opt<A>{M::lift(*a.carry_in), true};
+    } else {
+      carry = pipe_lookback(a, cur, epoch, agg_cur, sh);
+    }
+    phase_c(cur, s_cur, opt_combine(aop, carry, ex_cur));
+    if (nxt == kNoTile) break;
+    cur = nxt;
+    s_cur = s_next;
+    agg_cur = agg_next;
+    ex_cur = ex_next;
+    it = it_next;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Workspace + launch.
 
 template <class T, class S, class Op>
@@ -592,6 +943,33 @@ inline bool scan_force_regs() {
     return e && std::strcmp(e, "regs") == 0;
   }();
   return v;
+}
+
+inline bool scan_use_one_tile_kernel() {
+  static const bool v = [] {
+    const char* e = std::getenv("FORGE_SCAN_PATH");
+    return e && std::strcmp(e, "smem") == 0;
+  }();
+  return v;
+}
+
+// Persistent grid: #SM x resident CTAs of the pipelined kernel.
+template <class T, class S, class F, class Op, bool Inclusive>
+inline uint32_t scan_pipe_grid(uint64_t ntiles) {
+  static thread_local int cached_dev = -1, cached_occ = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    cudaFuncSetAttribute(scan_pipe_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kPipeDyn));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_pipe_kernel<T, S, F, Op, Inclusive>, kPipeThreads,
+                                                  kPipeDyn);
+    cached_occ = occ < 1 ? 1 : occ;
+    cached_dev = dev;
+  }
+  const uint64_t cap = uint64_t(device_props().sm_count) * cached_occ;
+  return uint32_t(ntiles < cap ? ntiles : cap);
 }
 
 template <class T, class S, class F, class Op, bool Inclusive>
@@ -637,6 +1015,16 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
     CUtensorMap tmap_out = tmap;
     const bool tstore = sizeof(S) == sizeof(T) && !scan_env_u32("FORGE_SCAN_NO_TMA_STORE", 0) &&
                         make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
+    if (!scan_use_one_tile_kernel()) {
+      if (inclusive) {
+        const uint32_t g = scan_pipe_grid<T, S, F, Op, true>(a.ntiles);
+        scan_pipe_kernel<T, S, F, Op, true><<<g, kPipeThreads, kPipeDyn, stream>>>(a, tmap, tmap_out, tstore);
+      } else {
+        const uint32_t g = scan_pipe_grid<T, S, F, Op, false>(a.ntiles);
+        scan_pipe_kernel<T, S, F, Op, false><<<g, kPipeThreads, kPipeDyn, stream>>>(a, tmap, tmap_out, tstore);
+      }
+      return cudaGetLastError();
+    }
     if (inclusive) {
       scan_smem_prepare<T, S, F, Op, true>();
       scan_smem_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap, tmap_out, tstore);
