@@ -878,7 +878,9 @@ __global__ void __launch_bounds__(kPipeThreads)
   if (cur == kNoTile) return;
   const uint32_t epoch = s_epoch;
   C agg_cur;
+  trace_mark(a.trace, cur, 0);
   Opt<A> ex_cur = phase_a(cur, 0, epoch, agg_cur);
+  trace_mark(a.trace, cur, 1);
   for (;;) {
     const uint32_t it_next = it + 1;
     const int s_next = int(it_next % kPipeStages);
@@ -886,15 +888,22 @@ __global__ void __launch_bounds__(kPipeThreads)
     const uint32_t nxt = ring[s_next];
     C agg_next{};
     Opt<A> ex_next{A{}, false};
-    if (nxt != kNoTile) ex_next = phase_a(nxt, s_next, epoch, agg_next);
+    if (nxt != kNoTile) {
+      trace_mark(a.trace, nxt, 0);
+      ex_next = phase_a(nxt, s_next, epoch, agg_next);
+      trace_mark(a.trace, nxt, 1);
+    }
     // look-back of the current tile
     Opt<A> carry{A{}, false};
+    trace_mark(a.trace, cur, 2);
     if (cur == 0) {
       if (a.carry_in) carry = Opt<A>{M::lift(*a.carry_in), true};
     } else {
       carry = pipe_lookback(a, cur, epoch, agg_cur, sh);
     }
+    trace_mark(a.trace, cur, 3);
     phase_c(cur, s_cur, opt_combine(aop, carry, ex_cur));
+    trace_mark(a.trace, cur, 4);
     if (nxt == kNoTile) break;
     cur = nxt;
     s_cur = s_next;
