@@ -954,10 +954,12 @@ inline bool scan_force_regs() {
   return v;
 }
 
+// Default fast path: one TMA tile per CTA (measured fastest, profiles/);
+// FORGE_SCAN_PATH=pipe selects the persistent pipelined kernel.
 inline bool scan_use_one_tile_kernel() {
   static const bool v = [] {
     const char* e = std::getenv("FORGE_SCAN_PATH");
-    return e && std::strcmp(e, "smem") == 0;
+    return !(e && std::strcmp(e, "pipe") == 0);
   }();
   return v;
 }
