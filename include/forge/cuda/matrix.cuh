@@ -262,6 +262,49 @@ __global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, 
   }
   __syncthreads();
   if (!s_last) return;
+  // Fold the split partials of this thread's rows in split order.  Full row
+  // groups read each split's VE partials with coalesced strong vector loads,
+  // four splits in flight.
+  if (i0 + VE <= a.n && (sizeof(S) * VE) % 16 == 0 && is_aligned(a.partials + i0, 16) &&
+      (uint64_t(a.n) * sizeof(S)) % 16 == 0) {
+    constexpr int W = int(sizeof(S) * VE) / 16;  // 16-byte words per row group
+    auto load_group = [&](uint32_t q, S (&dst)[VE]) {
+      uint4 w[W];
+      const uint4* p = reinterpret_cast<const uint4*>(a.partials + uint64_t(q) * a.n + i0);
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z), "=r"(w[k].w)
+                     : "l"(p + k)
+                     : "memory");
+      memcpy(dst, w, sizeof(S) * VE);
+    };
+    S acc2[VE];
+    load_group(0, acc2);
+    uint32_t q = 1;
+    for (; q + 4 <= a.ks; q += 4) {
+      S g[4][VE];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_group(q + u, g[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc2[e] = a.op(acc2[e], g[u][e]);
+    }
+    for (; q < a.ks; ++q) {
+      S g[VE];
+      load_group(q, g);
+#pragma unroll
+      for (int e = 0; e < VE; ++e) acc2[e] = a.op(acc2[e], g[e]);
+    }
+    if (is_aligned(a.z + i0, 32) && (sizeof(S) * VE) % 32 == 0) {
+      store_items<S, VE>(a.z + i0, acc2);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VE; ++e) a.z[i0 + e] = acc2[e];
+    }
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < VE; ++e) {
     const uint64_t i = i0 + e;
