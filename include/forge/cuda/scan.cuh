@@ -913,6 +913,12 @@ __global__ void __launch_bounds__(kPipeThreads)
   }
 }
 
+}  // namespace forge::cuda
+
+#include "forge/cuda/scan_ws.cuh"  // warp-specialised kernel (uses the machinery above)
+
+namespace forge::cuda {
+
 // ---------------------------------------------------------------------------
 // Workspace + launch.
 
@@ -956,6 +962,35 @@ inline bool scan_force_regs() {
 
 // Default fast path: one TMA tile per CTA (measured fastest, profiles/);
 // FORGE_SCAN_PATH=pipe selects the persistent pipelined kernel.
+// 0 = one tile per CTA, 1 = pipelined, 2 = warp-specialised.
+inline int scan_path() {
+  static const int v = [] {
+    const char* e = std::getenv("FORGE_SCAN_PATH");
+    if (e && std::strcmp(e, "ws") == 0) return 2;
+    if (e && std::strcmp(e, "pipe") == 0) return 1;
+    return 0;
+  }();
+  return v;
+}
+
+template <class T, class S, class F, class Op, bool Inclusive>
+inline uint32_t scan_ws_grid(uint64_t ntiles) {
+  static thread_local int cached_dev = -1, cached_occ = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    cudaFuncSetAttribute(scan_ws_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(ws_dyn_bytes<T, S, Op>()));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_ws_kernel<T, S, F, Op, Inclusive>, kWsThreads,
+                                                  ws_dyn_bytes<T, S, Op>());
+    cached_occ = occ < 1 ? 1 : occ;
+    cached_dev = dev;
+  }
+  const uint64_t cap = uint64_t(device_props().sm_count) * cached_occ;
+  return uint32_t(ntiles < cap ? ntiles : cap);
+}
+
 inline bool scan_use_one_tile_kernel() {
   static const bool v = [] {
     const char* e = std::getenv("FORGE_SCAN_PATH");
@@ -1026,6 +1061,18 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
     CUtensorMap tmap_out = tmap;
     const bool tstore = sizeof(S) == sizeof(T) && !scan_env_u32("FORGE_SCAN_NO_TMA_STORE", 0) &&
                         make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
+    if (scan_path() == 2) {
+      if (inclusive) {
+        const uint32_t g = scan_ws_grid<T, S, F, Op, true>(a.ntiles);
+        scan_ws_kernel<T, S, F, Op, true>
+            <<<g, kWsThreads, ws_dyn_bytes<T, S, Op>(), stream>>>(a, tmap, tmap_out, tstore);
+      } else {
+        const uint32_t g = scan_ws_grid<T, S, F, Op, false>(a.ntiles);
+        scan_ws_kernel<T, S, F, Op, false>
+            <<<g, kWsThreads, ws_dyn_bytes<T, S, Op>(), stream>>>(a, tmap, tmap_out, tstore);
+      }
+      return cudaGetLastError();
+    }
     if (!scan_use_one_tile_kernel()) {
       if (inclusive) {
         const uint32_t g = scan_pipe_grid<T, S, F, Op, true>(a.ntiles);
