@@ -37,3 +37,18 @@ if what == "scan":
             out[name + "_bad"] = bad
         del src, dst
 print(json.dumps({"path": os.environ.get("FORGE_SCAN_PATH", "tile"), what: out}))
+if what == "mapreduce":
+    n = 1 << 30
+    for name, op in (("f32_sumsq", capi.F32_SUMSQ), ("i32_max", capi.I32_MAX), ("uf8_f32_sum", capi.UF8_F32_SUM)):
+        src = dev.empty(op, n); dev.fill_synthetic(op, src, n, 7)
+        out_t = torch.zeros(16, dtype=torch.uint8, device="cuda")
+        ms = t(lambda: dev.mapreduce(op, src, n, out_t, ws))
+        out[name] = round(n * op_info(op)["t_size"] / ms / 1e6, 1)
+        if check:
+            from oracle import oracle as orc
+            import numpy as np
+            got = out_t.cpu().numpy().view(np.uint8)[: orc.s_dtype(op).itemsize].view(orc.s_dtype(op))
+            want, ex, sc = orc.mapreduce_synthetic(op, n, 7)
+            out[name + "_ok"] = bool(orc.within(op, got, ex, sc, 1e-5)[0]) if orc.ncomp(op) else bool(got[0] == want)
+        del src
+    print(json.dumps({"mapreduce": out}))
