@@ -1052,9 +1052,12 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
     const uint32_t w = scan_state_words_override();
     if (w >= TileStateIO<typename CarryTraits<S, Op>::C>::STRIDE && w <= a.state_stride) a.state_stride = w;
   }
+  // The TMA tile kernels are instantiated only for power-of-two element sizes
+  // up to 16 bytes (whole items per 16-byte chunk); other types take the
+  // register kernel.
+  if constexpr (smem_scan_type_ok<T>()) {
   CUtensorMap tmap;
-  const bool smem = smem_scan_type_ok<T>() && !scan_force_regs() && src_stride == 1 && dst_stride == 1 &&
-                    n >= WsT::kTileSmem &&
+  const bool smem = !scan_force_regs() && src_stride == 1 && dst_stride == 1 && n >= WsT::kTileSmem &&
                     make_rows128_map(&tmap, src, (n * sizeof(T)) / kRowBytes, uint32_t(kScanThreads));
   if (smem) {
     a.ntiles = uint32_t(ceil_div(n, WsT::kTileSmem));
@@ -1090,13 +1093,14 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
       scan_smem_prepare<T, S, F, Op, false>();
       scan_smem_kernel<T, S, F, Op, false><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap, tmap_out, tstore);
     }
-  } else {
-    a.ntiles = uint32_t(ceil_div(n, WsT::kTileGeneral));
-    if (inclusive)
-      scan_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, 0, stream>>>(a);
-    else
-      scan_kernel<T, S, F, Op, false><<<a.ntiles, kScanThreads, 0, stream>>>(a);
+    return cudaGetLastError();
   }
+  }
+  a.ntiles = uint32_t(ceil_div(n, WsT::kTileGeneral));
+  if (inclusive)
+    scan_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, 0, stream>>>(a);
+  else
+    scan_kernel<T, S, F, Op, false><<<a.ntiles, kScanThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
