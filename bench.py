@@ -202,20 +202,28 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
     from paper_2603_18695_b200 import capi, dev
     from paper_2603_18695_b200 import forge as F
 
+    # one process per GPU; FORGE_DIST_BACKEND=gloo lets a 1-GPU box run the
+    # N>1 code path with every rank on cuda:0 (test only — NCCL is the product)
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("FORGE_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
+    from paper_2603_18695_b200.sharded import _all_gather_bytes
     stream = torch.cuda.current_stream()
-    n = args.n
+    n = args.elems
     ops = (capi.F32_SUMSQ, capi.I32_MAX)
     bufs = {}
     for i, op in enumerate(ops):
         bufs[op] = dev.empty(op, n)
         dev.fill_synthetic(op, bufs[op], n, seed=0x5EED0010 + i, index_base=rank * n)
     outs = {op: torch.zeros(16, dtype=torch.uint8, device="cuda") for op in ops}
-    gath = {op: torch.zeros(16 * world, dtype=torch.uint8, device="cuda") for op in ops}
+    ssz = {op: F.op_info(op)["s_size"] for op in ops}
     final = {op: torch.zeros(16, dtype=torch.uint8, device="cuda") for op in ops}
     wss = {op: dev.Workspace() for op in ops}
     kern_ev = []  # (start, end) events around each mapreduce launch (roofline)
@@ -230,8 +238,9 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
                 e1.record(stream)
                 kern_ev.append((e0, e1))
             if world > 1:
-                dist.all_gather_into_tensor(gath[op], outs[op][:4].contiguous())
-                dev.fold(op, gath[op], world, final[op], stream=stream)
+                # partials exchange: sizeof(S) bytes per rank, folded in rank order on the device
+                gath = _all_gather_bytes(outs[op][: ssz[op]], world)
+                dev.fold(op, gath, world, final[op], stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -248,9 +257,11 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
             step()
         t1.record(stream)
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
     ms = t0.elapsed_time(t1)
     if dist:
-        tt = torch.tensor([ms], device="cuda")
+        tt = torch.tensor([ms], device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     bytes_step = sum(n * F.op_info(op)["t_size"] for op in ops)
@@ -428,7 +439,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["forge", "reference"], default="forge")
-    ap.add_argument("--n", type=int, default=N_C2)
+    ap.add_argument("--elems", type=int, default=N_C2, help="elements per GPU per op")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-breakdown", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "forge/cuda/reduce.cuh"
+#include "forge/cuda/tma.cuh"
 
 namespace forge::cuda {
 
@@ -56,6 +57,81 @@ __global__ void __launch_bounds__(kCopyThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk copy (the B200 path of vcopy for 16-byte-congruent buffers): one
+// CTA per SM, one elected thread streams 32 KB chunks global -> shared ->
+// global with cp.async.bulk through a ring of kBulkStages stages, keeping
+// kBulkStages-1 loads in flight (~160 KB per SM, the Little's-law depth for
+// read+write at HBM latency) while the stores drain behind them.  No register
+// staging and no per-element instructions: the copy engine moves the bytes.
+
+constexpr uint32_t kBulkChunk = 32u << 10;
+constexpr int kBulkStages = 6;
+constexpr uint32_t kBulkDyn = kBulkStages * kBulkChunk;
+
+__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* ssrc, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+// Copies `bytes` (multiple of 16) from src to dst (both 16-byte aligned).
+__global__ void __launch_bounds__(32, 1)
+    bulk_copy_kernel(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, uint64_t bytes) {
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  __shared__ __align__(8) uint64_t full[kBulkStages];
+  if (threadIdx.x != 0) return;
+  const uint64_t nchunks = ceil_div(bytes, kBulkChunk);
+  const uint64_t G = gridDim.x;
+  const uint64_t mine = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / G + 1 : 0;
+  if (mine == 0) return;
+  const uint64_t pol = policy_evict_first();
+  for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+  fence_mbar_init();
+  auto chunk_bytes = [&](uint64_t k) {
+    const uint64_t off = (blockIdx.x + k * G) * uint64_t(kBulkChunk);
+    return uint32_t(bytes - off < kBulkChunk ? bytes - off : kBulkChunk);
+  };
+  auto issue_load = [&](uint64_t k) {
+    const int s = int(k % kBulkStages);
+    const uint64_t off = (blockIdx.x + k * G) * uint64_t(kBulkChunk);
+    const uint32_t b = chunk_bytes(k);
+    mbar_arrive_expect_tx(&full[s], b);
+    bulk_load_1d(bulk_smem + size_t(s) * kBulkChunk, src + off, b, &full[s], pol);
+  };
+  for (uint64_t k = 0; k < mine && k < uint64_t(kBulkStages); ++k) issue_load(k);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const int s = int(k % kBulkStages);
+    mbar_wait(&full[s], uint32_t(k / kBulkStages) & 1u);
+    const uint64_t off = (blockIdx.x + k * G) * uint64_t(kBulkChunk);
+    bulk_store_1d(dst + off, bulk_smem + size_t(s) * kBulkChunk, chunk_bytes(k), pol);
+    tma_store_commit();
+    // refill the stage of chunk k-1 once its store has read shared memory
+    if (k >= 1 && k - 1 + kBulkStages < mine) {
+      bulk_wait_read<1>();
+      issue_load(k - 1 + kBulkStages);
+    }
+  }
+  bulk_wait_read<0>();
+}
+
 template <class T>
 __global__ void strided_copy_kernel(const T* src, uint64_t sstride, T* dst, uint64_t dstride,
                                     uint64_t n) {
@@ -78,6 +154,22 @@ cudaError_t launch_vcopy(const T* src, T* dst, uint64_t n, cudaStream_t stream) 
   constexpr int VB = mr_vec_elems<T>() * int(sizeof(T));
   const bool vec = (reinterpret_cast<uintptr_t>(src) % VB) == (reinterpret_cast<uintptr_t>(dst) % VB) &&
                    (reinterpret_cast<uintptr_t>(src) % sizeof(T)) == 0;
+  const uint64_t bytes = n * sizeof(T);
+  static const bool no_bulk = std::getenv("FORGE_COPY_NO_BULK") != nullptr;
+  if (!no_bulk && bytes >= (8u << 20) && is_aligned(src, 16) && is_aligned(dst, 16) && bytes % 16 == 0) {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done_dev != dev) {
+      cudaFuncSetAttribute(bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBulkDyn));
+      done_dev = dev;
+    }
+    const uint64_t chunks = ceil_div(bytes, kBulkChunk);
+    const uint64_t sms = uint64_t(device_props().sm_count);
+    bulk_copy_kernel<<<uint32_t(chunks < sms ? chunks : sms), 32, kBulkDyn, stream>>>(
+        reinterpret_cast<const unsigned char*>(src), reinterpret_cast<unsigned char*>(dst), bytes);
+    return cudaGetLastError();
+  }
   vcopy_kernel<T, 4><<<copy_grid<T>(n), kCopyThreads, 0, stream>>>(src, dst, n, vec);
   return cudaGetLastError();
 }

@@ -50,9 +50,11 @@ namespace forge::cuda {
 
 constexpr int kScanThreads = 256;
 constexpr uint32_t kPartial = 1, kPrefix = 2;
-constexpr int kLookbackPerThread = 4;     // max polls per thread of the block-wide look-back
+constexpr int kLookbackPerThread = 4;     // max polls per thread of the block-wide look-back (pipe kernel)
+constexpr int kLookbackRows = 1;          // warp look-back: rows of 32 predecessors per round trip
 constexpr uint32_t kStateSlotWords = 32;  // 256-byte tile-state slots
 constexpr int kRowBytes = 128;            // smem kernel: bytes of T per thread row
+constexpr uint32_t kLookbackSkipProbe = 99;  // FORGE_SCAN_LOOKBACK value of the no-look-back probe
 
 template <class C>
 struct TileStateIO {
@@ -74,6 +76,32 @@ struct TileStateIO {
         st_relaxed_gpu_v2(p + i, lo_word, hi_word);
       }
     }
+  }
+
+  // Split read for callers that poll many states at once: issue every load
+  // first (load_raw), decode after — so the loads are in flight together.
+  static __device__ __forceinline__ void load_raw(const uint64_t* states, uint64_t tile, uint32_t stride,
+                                                  uint64_t (&raw)[STRIDE]) {
+    const uint64_t* p = states + tile * stride;
+    if constexpr (STRIDE == 1) {
+      raw[0] = ld_relaxed_gpu(p);
+    } else {
+#pragma unroll
+      for (int i = 0; i < STRIDE; i += 2) ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
+    }
+  }
+  static __device__ __forceinline__ uint32_t decode(const uint64_t (&raw)[STRIDE], uint32_t epoch, C& v) {
+    const uint32_t hi = uint32_t(raw[0] >> 32);
+    bool same = true;
+#pragma unroll
+    for (int i = 1; i < SW; ++i) same &= uint32_t(raw[i] >> 32) == hi;
+    const uint32_t kind = hi & 3u;
+    if (!same || kind == 0 || (hi >> 2) != (epoch & 0x3fffffffu)) return 0;
+    Words<C> w;
+#pragma unroll
+    for (int i = 0; i < SW; ++i) w.w[i] = uint32_t(raw[i]);
+    v = from_words<C>(w);
+    return kind;
   }
 
   // Returns the kind (0 = not yet valid for this epoch) and the value.
@@ -136,12 +164,80 @@ template <class A, class C>
 struct ScanShared {
   Opt<A> warp[kScanThreads / kWarp];
   Opt<A> carry;
-  int first[kScanThreads / kWarp];  // block-wide look-back: nearest PREFIX per warp
-  Opt<C> lb[kScanThreads / kWarp];  // block-wide look-back: per-warp window folds
 };
 
 template <class S, class Op>
 using ScanSharedOf = ScanShared<typename ScanMath<S, Op>::A, typename ScanMath<S, Op>::C>;
+
+// Decoupled look-back by one warp (primitives.hpp:536-576), Q rows of 32
+// predecessors per L2 round trip: every lane issues its Q state loads together
+// (decode after issue, so they are in flight at once), re-polls only the
+// positions still INVALID, then finds the nearest PREFIX with one ballot per
+// row and folds everything newer than it with an ORDER-PRESERVING log-step
+// reduction (older tile always on the left; the reference folded serially,
+// :561-563).  Returns the carry (all lanes).
+// Measured (tools/trace_scan.py, f32 2^28): the nearest PREFIX sits ~100 tiles
+// back under load; Q = 1 takes 3.4 rounds of 1.65 us, Q = 4 takes 2.0 rounds of
+// 3.5 us — a round's latency grows with the polls because ~800 resident tiles
+// poll the same few hundred newest state lines — so Q = 1 stays the default.
+template <int Q, class IO, class C, class COp>
+__device__ __forceinline__ Opt<C> warp_lookback(const uint64_t* states, uint32_t stride, uint32_t epoch,
+                                                int64_t tile, const COp& cop, uint64_t* trace, uint64_t trace_tile) {
+  constexpr uint32_t kEmpty = 4;  // position before tile 0
+  const unsigned lane = lane_id();
+  Opt<C> carry{C{}, false};
+  int64_t hi = tile;
+  uint32_t rounds = 0;
+  for (;;) {
+    ++rounds;
+    C val[Q];
+    uint32_t kind[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      kind[q] = hi - 1 - int64_t(q * kWarp + lane) < 0 ? kEmpty : 0u;
+      val[q] = C{};
+    }
+    for (;;) {
+      uint64_t raw[Q][IO::STRIDE];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (kind[q] == 0) IO::load_raw(states, uint64_t(hi - 1 - int64_t(q * kWarp + lane)), stride, raw[q]);
+      bool all = true;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (kind[q] == 0) {
+          kind[q] = IO::decode(raw[q], epoch, val[q]);
+          all &= kind[q] != 0;
+        }
+      }
+      if (__all_sync(kFullMask, all)) break;
+    }
+    int P = Q * kWarp;  // position of the nearest PREFIX (0 = tile hi-1)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const unsigned pm = __ballot_sync(kFullMask, kind[q] == kPrefix);
+      if (P == Q * kWarp && pm) P = q * kWarp + __ffs(int(pm)) - 1;
+    }
+    Opt<C> win{C{}, false};
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (q * kWarp <= P) {
+        Opt<C> v{val[q], int(q * kWarp + lane) <= P && kind[q] != kEmpty};
+#pragma unroll
+        for (unsigned d = 1; d < kWarp; d <<= 1) {
+          Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
+          if (lane + d < kWarp) v = opt_combine(cop, got, v);
+        }
+        win = opt_combine(cop, shfl_idx_opt(v, 0), win);  // row q is older than rows < q
+      }
+    }
+    carry = opt_combine(cop, win, carry);
+    if (P < Q * kWarp) break;
+    hi -= Q * kWarp;
+  }
+  if (trace && lane == 0) trace[trace_tile * 8 + 6] = rounds;
+  return carry;
+}
 
 // Reads the epoch, claims the next tile (acq_rel ticket); the last of the
 // `ntiles` claims resets the ticket and advances the epoch (see header).
@@ -203,93 +299,10 @@ __device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> block_exclusive_pref
     const C agg_c = M::to_c(agg.v);
     if (threadIdx.x == 0) IO::write(a.states, tile, a.state_stride, epoch, kPartial, agg_c);
     Opt<C> carry{C{}, false};  // meaningful in thread 0
-    if (a.lookback == 0) {
-      if (warp == 0) {
-        int64_t hi = int64_t(tile);
-        uint32_t windows = 0, polls = 0;
-        for (;;) {
-          ++windows;
-          const int64_t j = hi - 1 - int64_t(lane);
-          C val{};
-          uint32_t kind = 0;
-          if (j >= 0) {
-            while ((kind = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val)) == 0) {
-              if (a.trace) ++polls;
-            }
-          }
-          if (a.trace && lane == 0) {
-            a.trace[tile * 8 + 6] = windows;
-            a.trace[tile * 8 + 7] = __reduce_max_sync(kFullMask, polls) + windows;
-          } else if (a.trace) {
-            __reduce_max_sync(kFullMask, polls);
-          }
-          const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
-          const int pl = pm ? __ffs(int(pm)) - 1 : kWarp - 1;
-          // Lanes 0..pl hold tiles hi-1 .. hi-1-pl (newest first): fold them with
-          // the older (higher) lane on the LEFT of every combine.
-          Opt<C> v{val, int(lane) <= pl && j >= 0};
-#pragma unroll
-          for (unsigned d = 1; d < kWarp; d <<= 1) {
-            Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
-            if (lane + d < kWarp) v = opt_combine(cop, got, v);
-          }
-          const Opt<C> window{shfl_idx(v.v, 0), __shfl_sync(kFullMask, int(v.has), 0) != 0};
-          carry = opt_combine(cop, window, carry);
-          if (pm) break;
-          hi -= kWarp;
-        }
-      }
-    } else {
-      constexpr int LB = kLookbackPerThread;
-      const int lbn = int(a.lookback < uint32_t(LB) ? a.lookback : uint32_t(LB));
-      const int WIN = kScanThreads * lbn;
-      int64_t hi = int64_t(tile);
-      for (;;) {
-        C val[LB];
-        uint32_t kind[LB];
-        int first = WIN;
-#pragma unroll
-        for (int q = 0; q < LB; ++q) {
-          kind[q] = 0;
-          val[q] = C{};
-          const int64_t j = hi - 1 - int64_t(threadIdx.x) * lbn - q;
-          if (q < lbn && j >= 0) {
-            while ((kind[q] = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val[q])) == 0) {
-            }
-          }
-          if (kind[q] == kPrefix && first == WIN) first = int(threadIdx.x) * lbn + q;
-        }
-        const unsigned pm = __ballot_sync(kFullMask, first < WIN);
-        const int wfirst = __shfl_sync(kFullMask, first, pm ? __ffs(int(pm)) - 1 : 0);
-        if (lane == 0) sh.first[warp] = pm ? wfirst : WIN;
-        __syncthreads();
-        int pl = WIN;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
-        const bool found = pl < WIN;
-        Opt<C> v{C{}, false};
-#pragma unroll
-        for (int q = LB - 1; q >= 0; --q) {
-          const int pos = int(threadIdx.x) * lbn + q;
-          if (kind[q] != 0 && pos <= pl) v = opt_combine(cop, v, Opt<C>{val[q], true});
-        }
-#pragma unroll
-        for (unsigned d = 1; d < kWarp; d <<= 1) {
-          Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
-          if (lane + d < kWarp) v = opt_combine(cop, got, v);
-        }
-        if (lane == 0) sh.lb[warp] = v;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          Opt<C> window{C{}, false};
-#pragma unroll
-          for (int w = NW - 1; w >= 0; --w) window = opt_combine(cop, window, sh.lb[w]);
-          carry = opt_combine(cop, window, carry);
-        }
-        if (found) break;
-        hi -= WIN;
-        __syncthreads();  // sh.first / sh.lb are rewritten by the next round
-      }
+    if (a.lookback == kLookbackSkipProbe) {
+      // development ceiling probe (FORGE_SCAN_LOOKBACK=99): no look-back, WRONG results
+    } else if (warp == 0) {
+      carry = warp_lookback<kLookbackRows, IO, C>(a.states, a.state_stride, epoch, int64_t(tile), cop, a.trace, tile);
     }
     if (threadIdx.x == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
@@ -400,8 +413,15 @@ constexpr uint32_t kSmemScanDyn = kSmemTileBytes + 1024;                 // + sw
 // `tmap_out` (used when tma_store) views dst as 128-byte rows; only for
 // sizeof(S) == sizeof(T), where each output chunk overwrites its input chunk
 // in shared memory and the finished tile leaves with one TMA tensor store.
+// Resident CTAs per SM the smem kernel is compiled for: 6 x 33 KB of tile
+// (Little's law) needs <= 40 registers; wide carries get 4.
+template <class S, class Op>
+constexpr int scan_smem_min_blocks() {
+  return sizeof(typename ScanMath<S, Op>::C) <= 8 ? 6 : 4;
+}
+
 template <class T, class S, class F, class Op, bool Inclusive>
-__global__ void __launch_bounds__(kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op>())
     scan_smem_kernel(const ScanArgs<T, S, F, Op> a, const __grid_constant__ CUtensorMap tmap,
                      const __grid_constant__ CUtensorMap tmap_out, bool tma_store) {
   using M = ScanMath<S, Op>;
@@ -915,7 +935,9 @@ __global__ void __launch_bounds__(kPipeThreads)
 
 }  // namespace forge::cuda
 
-#include "forge/cuda/scan_ws.cuh"  // warp-specialised kernel (uses the machinery above)
+#include "forge/cuda/scan_ws.cuh"       // warp-specialised kernel (uses the machinery above)
+#include "forge/cuda/scan_cluster.cuh"  // cluster-tiled kernel (uses the machinery above)
+#include "forge/cuda/scan_chain.cuh"    // persistent kernel with a carry chain (uses the machinery above)
 
 namespace forge::cuda {
 
@@ -966,6 +988,7 @@ inline bool scan_force_regs() {
 inline int scan_path() {
   static const int v = [] {
     const char* e = std::getenv("FORGE_SCAN_PATH");
+    if (e && std::strcmp(e, "chain") == 0) return 3;
     if (e && std::strcmp(e, "ws") == 0) return 2;
     if (e && std::strcmp(e, "pipe") == 0) return 1;
     return 0;
@@ -1018,6 +1041,88 @@ inline uint32_t scan_pipe_grid(uint64_t ntiles) {
   return uint32_t(ntiles < cap ? ntiles : cap);
 }
 
+// CTAs per look-back tile of the cluster kernel (FORGE_SCAN_CLUSTER; 1 = the
+// one-tile-per-CTA kernel).
+inline uint32_t scan_cluster_size() {
+  static const uint32_t v = [] {
+    uint32_t k = scan_env_u32("FORGE_SCAN_CLUSTER", 1);
+    return k == 0 ? 1u : (k > uint32_t(kMaxScanCluster) ? uint32_t(kMaxScanCluster) : k);
+  }();
+  return v;
+}
+
+template <class T, class S, class F, class Op, bool Inclusive>
+cudaError_t launch_scan_cluster(const ScanArgs<T, S, F, Op>& a, const CUtensorMap& tmap,
+                                const CUtensorMap& tmap_out, bool tstore, uint32_t K, uint32_t nsub,
+                                cudaStream_t stream) {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto kern = scan_cluster_kernel<T, S, F, Op, Inclusive>;
+  if (done_dev != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemScanDyn));
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         int(scan_env_u32("FORGE_SCAN_CARVEOUT", 100)));
+    done_dev = dev;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(uint32_t(ceil_div(nsub, K)) * K);
+  cfg.blockDim = dim3(kScanThreads);
+  cfg.dynamicSmemBytes = kSmemScanDyn;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = K;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, tmap, tmap_out, tstore);
+}
+
+// Persistent carry-chain kernel: cooperative grid of #SM x resident CTAs,
+// FORGE_SCAN_CHAIN_CTAS (1|2) per SM, as many ring stages as fit
+// (FORGE_SCAN_STAGES caps), lag D (FORGE_SCAN_LAG) between reduce and scan.
+template <class T, class S, class F, class Op, bool Inclusive>
+cudaError_t launch_scan_chain(const ScanArgs<T, S, F, Op>& a, const CUtensorMap& tmap, const CUtensorMap& tmap_out,
+                              bool tstore, cudaStream_t stream) {
+  using L = ChainLayout<S, Op>;
+  auto kern = scan_chain_kernel<T, S, F, Op, Inclusive>;
+  static thread_local int cached_dev = -1;
+  static thread_local int ns = 0, lag = 0, occ = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cached_dev != dev) {
+    const uint32_t per_sm = scan_env_u32("FORGE_SCAN_CHAIN_CTAS", 1) >= 2 ? 2u : 1u;
+    const uint32_t budget = (per_sm == 1 ? 232448u : 114688u) - 2048u;  // dynamic smem per CTA
+    int fit = int((budget - 1024u) / L::kStageBytes);
+    fit = fit > kChainMaxStages ? kChainMaxStages : fit;
+    const int req = int(scan_env_u32("FORGE_SCAN_STAGES", 0));
+    ns = req >= 2 && req < fit ? req : fit;
+    const int half = ns / 2 > 1 ? ns / 2 : 1;
+    const int dflt_lag = ns - 1 - half > 1 ? ns - 1 - half : 1;
+    const int lreq = int(scan_env_u32("FORGE_SCAN_LAG", 0));
+    lag = lreq >= 1 && lreq <= ns - 1 ? lreq : dflt_lag;
+    if (ns < lag + 1) return cudaErrorInvalidConfiguration;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::dyn_bytes(ns)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kChainThreads, L::dyn_bytes(ns));
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    cached_dev = dev;
+  }
+  const uint64_t cap = uint64_t(device_props().sm_count) * uint64_t(occ);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(uint32_t(a.ntiles < cap - 1 ? a.ntiles : cap - 1) + 1);  // + the chain CTA
+  cfg.blockDim = dim3(kChainThreads);
+  cfg.dynamicSmemBytes = L::dyn_bytes(ns);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency is what guarantees progress
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, tmap, tmap_out, tstore, ns, lag);
+}
+
 template <class T, class S, class F, class Op, bool Inclusive>
 inline void scan_smem_prepare() {
   static thread_local int done_dev = -1;
@@ -1064,6 +1169,20 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
     CUtensorMap tmap_out = tmap;
     const bool tstore = sizeof(S) == sizeof(T) && !scan_env_u32("FORGE_SCAN_NO_TMA_STORE", 0) &&
                         make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
+    if (scan_path() == 3) {
+      const cudaError_t e = inclusive ? launch_scan_chain<T, S, F, Op, true>(a, tmap, tmap_out, tstore, stream)
+                                      : launch_scan_chain<T, S, F, Op, false>(a, tmap, tmap_out, tstore, stream);
+      return e != cudaSuccess ? e : cudaGetLastError();
+    }
+    const uint32_t K = scan_cluster_size();
+    if (scan_path() == 0 && K > 1) {
+      const uint32_t nsub = a.ntiles;
+      a.ntiles = uint32_t(ceil_div(nsub, K));  // look-back tiles = clusters
+      const cudaError_t e =
+          inclusive ? launch_scan_cluster<T, S, F, Op, true>(a, tmap, tmap_out, tstore, K, nsub, stream)
+                    : launch_scan_cluster<T, S, F, Op, false>(a, tmap, tmap_out, tstore, K, nsub, stream);
+      return e != cudaSuccess ? e : cudaGetLastError();
+    }
     if (scan_path() == 2) {
       if (inclusive) {
         const uint32_t g = scan_ws_grid<T, S, F, Op, true>(a.ntiles);

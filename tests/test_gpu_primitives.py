@@ -348,7 +348,7 @@ def test_matrix_empty_reduction_fills_identity(m):
 # ---------------------------------------------------------------------------
 # vcopy
 
-@pytest.mark.parametrize("n", [0, 1, 3, 31, 4099, 1_000_003])
+@pytest.mark.parametrize("n", [0, 1, 3, 31, 4099, 1_000_003, 4_000_004])
 @pytest.mark.parametrize("desc,dtype", [("f32", np.float32), ("u8", np.uint8), ("f64", np.float64),
                                         ("struct(u8@0,f64@8,u16@16;size=24)", np.dtype((np.void, 24)))])
 def test_vcopy(m, n, desc, dtype):
@@ -362,3 +362,19 @@ def test_vcopy(m, n, desc, dtype):
     assert rep.ok
     if n:
         assert np.array_equal(m.read(b, n, dtype).view(np.uint8), src.view(np.uint8))
+
+
+@pytest.mark.parametrize("off_a,off_b", [(0, 0), (4, 8), (1, 1), (1, 2)])
+def test_vcopy_offsets_bulk_sizes(m, off_a, off_b):
+    """>= 8 MiB copies take the TMA bulk path when both views are 16-byte
+    aligned (offsets 0/4/8 f32), the vector path otherwise; chunk tails included."""
+    n = (3 << 20) + 4 * 1237
+    rng = np.random.default_rng(off_a * 7 + off_b)
+    src = rng.standard_normal(n).astype(np.float32)
+    a = m.create_buffer("f32", n + 16)
+    b = m.create_buffer("f32", n + 16)
+    m.write(a, np.concatenate([np.zeros(off_a, np.float32), src]))
+    rep = F.vcopy(m, F.View(a, off_a, n, 1), F.View(b, off_b, n, 1), 4)
+    assert rep.ok
+    got = m.read(b, n + off_b, np.float32)[off_b:]
+    assert np.array_equal(got.view(np.uint32), src.view(np.uint32))

@@ -35,6 +35,8 @@ d["claims_per_us_mid"] = float(len(st) / (st[-1] - st[0]) * 1e3)
 print(json.dumps(d, indent=1))
 w = raw[:, 6]; p = raw[:, 7]
 lb = (ph[:, 3] - ph[:, 2]) / 1e3
-print(json.dumps({"windows_mean": float(w[1:].mean()), "windows_p90": float(np.percentile(w[1:], 90)),
-                  "poll_rounds_mean": float(p[1:].mean()), "poll_rounds_p90": float(np.percentile(p[1:], 90)),
-                  "us_per_poll_round": float((lb[1:] / np.maximum(p[1:], 1)).mean())}))
+sel = w > 0  # look-back owners (every tile; the cluster kernel: leader sub-tiles)
+print(json.dumps({"lookback_owners": int(sel.sum()), "windows_mean": float(w[sel].mean()),
+                  "windows_p90": float(np.percentile(w[sel], 90)),
+                  "poll_rounds_mean": float(p[sel].mean()),
+                  "us_per_window": float((lb[sel] / np.maximum(w[sel], 1)).mean())}))
