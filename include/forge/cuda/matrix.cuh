@@ -353,7 +353,12 @@ template <class T>
 inline GemvPlan plan_gemv(uint64_t n, uint64_t p) {
   constexpr int VE = gemv_vec_elems<T>();
   const uint64_t row_blocks = ceil_div(n, uint64_t(kMatThreads) * VE);
-  const uint64_t target_blocks = uint64_t(device_props().sm_count) * 4;
+  static const uint64_t per_sm = [] {
+    const char* e = std::getenv("FORGE_GEMV_BLOCKS_PER_SM");  // experiment knob
+    const uint64_t v = e ? std::strtoull(e, nullptr, 10) : 3;  // measured best of 1..8 at 16384^2
+    return v < 1 ? 1 : v;
+  }();
+  const uint64_t target_blocks = uint64_t(device_props().sm_count) * per_sm;
   uint64_t ks = row_blocks >= target_blocks ? 1 : ceil_div(target_blocks, row_blocks);
   const uint64_t max_ks = ceil_div(p, 16);  // >= 16 columns per split
   if (ks > max_ks) ks = max_ks;

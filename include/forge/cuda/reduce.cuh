@@ -264,10 +264,25 @@ __global__ void __launch_bounds__(kReduceThreads)
   __syncthreads();
   if (!s_last) return;
 
-  // Last block: fold the partials (deterministic tree for a fixed grid).
+  // Last block: fold the partials (deterministic tree for a fixed grid), with
+  // kFoldBatch partial loads in flight per thread.
+  constexpr int kFoldBatch = 8;
   Opt<S> v{S{}, false};
-  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kReduceThreads) {
-    if (ld_relaxed_gpu(a.part_has + b)) v = opt_combine(a.op, v, Opt<S>{ld_strong(a.partials + b), true});
+  for (uint32_t b0 = threadIdx.x; b0 < gridDim.x; b0 += kReduceThreads * kFoldBatch) {
+    uint32_t hs[kFoldBatch];
+    S ps[kFoldBatch];
+#pragma unroll
+    for (int q = 0; q < kFoldBatch; ++q) {
+      const uint32_t b = b0 + uint32_t(q) * kReduceThreads;
+      hs[q] = 0;
+      if (b < gridDim.x) {
+        hs[q] = ld_relaxed_gpu(a.part_has + b);
+        ps[q] = ld_strong(a.partials + b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kFoldBatch; ++q)
+      if (hs[q]) v = opt_combine(a.op, v, Opt<S>{ps[q], true});
   }
   Opt<S> total = block_reduce_comm(a.op, v, smem);
   if (threadIdx.x == 0) {
@@ -299,7 +314,15 @@ struct MapReduceWs {
   }
 };
 
-inline uint32_t mapreduce_max_grid() { return uint32_t(device_props().sm_count) * 4; }
+inline uint32_t mapreduce_blocks_per_sm() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("FORGE_MR_BLOCKS_PER_SM");  // experiment knob
+    const uint32_t k = e ? uint32_t(std::strtoul(e, nullptr, 10)) : 4u;
+    return k < 1 ? 1u : (k > 256 ? 256u : k);
+  }();
+  return v;
+}
+inline uint32_t mapreduce_max_grid() { return uint32_t(device_props().sm_count) * mapreduce_blocks_per_sm(); }
 
 template <class T>
 inline uint32_t mapreduce_grid(uint64_t n) {

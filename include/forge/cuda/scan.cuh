@@ -146,6 +146,7 @@ struct ScanArgs {
   uint32_t state_stride;  // 64-bit words per tile state slot
   uint32_t lookback;      // 0: warp 0 polls 32 predecessors; k: 256*k predecessors block-wide
   uint64_t* trace;        // optional per-tile phase timestamps (FORGE_SCAN_TRACE), else null
+  uint32_t backoff_ns;    // look-back: sleep between polls of INVALID states (FORGE_SCAN_BACKOFF_NS)
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -160,9 +161,11 @@ __device__ __forceinline__ void trace_mark(uint64_t* trace, uint64_t tile, int p
   if (trace && threadIdx.x == 0) trace[tile * 8 + phase] = global_ns();
 }
 
+constexpr int kMaxSubtiles = 2;  // 32 KB sub-tiles per CTA tile (smem kernel, scan_subtiles)
+
 template <class A, class C>
 struct ScanShared {
-  Opt<A> warp[kScanThreads / kWarp];
+  Opt<A> warp[kMaxSubtiles * kScanThreads / kWarp];
   Opt<A> carry;
 };
 
@@ -182,7 +185,8 @@ using ScanSharedOf = ScanShared<typename ScanMath<S, Op>::A, typename ScanMath<S
 // poll the same few hundred newest state lines — so Q = 1 stays the default.
 template <int Q, class IO, class C, class COp>
 __device__ __forceinline__ Opt<C> warp_lookback(const uint64_t* states, uint32_t stride, uint32_t epoch,
-                                                int64_t tile, const COp& cop, uint64_t* trace, uint64_t trace_tile) {
+                                                int64_t tile, const COp& cop, uint64_t* trace, uint64_t trace_tile,
+                                                uint32_t backoff_ns = 0) {
   constexpr uint32_t kEmpty = 4;  // position before tile 0
   const unsigned lane = lane_id();
   Opt<C> carry{C{}, false};
@@ -211,6 +215,7 @@ __device__ __forceinline__ Opt<C> warp_lookback(const uint64_t* states, uint32_t
         }
       }
       if (__all_sync(kFullMask, all)) break;
+      if (backoff_ns) __nanosleep(backoff_ns);
     }
     int P = Q * kWarp;  // position of the nearest PREFIX (0 = tile hi-1)
 #pragma unroll
@@ -257,30 +262,40 @@ __device__ __forceinline__ uint32_t claim_tile(const ScanArgs<T, S, F, Op>& a, u
 // EXCLUSIVE prefix of this thread (everything before its first item, carry and
 // earlier tiles included); `.has == false` only for the very first item of a
 // carry-less scan.
-template <class T, class S, class F, class Op>
-__device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> block_exclusive_prefix(
+//
+// R > 1: every thread holds R values — value r of thread t sits at position
+// r * kScanThreads + t of the tile (sub-tile r); all R * #warps warp totals are
+// scanned by warp 0 at once (R * 8 <= 32).
+template <int R, class T, class S, class F, class Op>
+__device__ __forceinline__ void block_exclusive_prefix(
     const ScanArgs<T, S, F, Op>& a, uint64_t tile, uint32_t epoch,
-    Opt<typename ScanMath<S, Op>::A> thread_total, ScanSharedOf<S, Op>& sh) {
+    const Opt<typename ScanMath<S, Op>::A> (&thread_total)[R], ScanSharedOf<S, Op>& sh,
+    Opt<typename ScanMath<S, Op>::A> (&ex)[R]) {
   using M = ScanMath<S, Op>;
   using A = typename M::A;
   using C = typename M::C;
   using IO = TileStateIO<C>;
   constexpr int NW = kScanThreads / kWarp;
+  static_assert(R >= 1 && R <= kMaxSubtiles && R * NW <= kWarp, "sub-tiles per CTA");
   const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
   auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
   auto cop = [&](const C& x, const C& y) { return M::CT::op(a.op, x, y); };
 
-  // ---- warp scan, cross-warp scan through shared memory (:501-516)
-  const Opt<A> incl = warp_scan_incl(aop, thread_total);
-  if (lane == kWarp - 1) sh.warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    Opt<A> w = lane < NW ? sh.warp[lane] : Opt<A>{A{}, false};
-    w = warp_scan_incl(aop, w);
-    if (lane < NW) sh.warp[lane] = w;
+  // ---- warp scans, cross-warp scan through shared memory (:501-516)
+  Opt<A> incl[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    incl[r] = warp_scan_incl(aop, thread_total[r]);
+    if (lane == kWarp - 1) sh.warp[r * NW + warp] = incl[r];
   }
   __syncthreads();
-  const Opt<A> agg = sh.warp[NW - 1];  // every tile holds >= 1 element
+  if (warp == 0) {
+    Opt<A> w = lane < R * NW ? sh.warp[lane] : Opt<A>{A{}, false};
+    w = warp_scan_incl(aop, w);
+    if (lane < R * NW) sh.warp[lane] = w;
+  }
+  __syncthreads();
+  const Opt<A> agg = sh.warp[R * NW - 1];  // every tile holds >= 1 element
 
   // ---- publish + decoupled look-back (:518-576)
   if (tile == 0) {
@@ -302,7 +317,8 @@ __device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> block_exclusive_pref
     if (a.lookback == kLookbackSkipProbe) {
       // development ceiling probe (FORGE_SCAN_LOOKBACK=99): no look-back, WRONG results
     } else if (warp == 0) {
-      carry = warp_lookback<kLookbackRows, IO, C>(a.states, a.state_stride, epoch, int64_t(tile), cop, a.trace, tile);
+      carry = warp_lookback<kLookbackRows, IO, C>(a.states, a.state_stride, epoch, int64_t(tile), cop, a.trace, tile,
+                                                  a.backoff_ns);
     }
     if (threadIdx.x == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
@@ -314,10 +330,14 @@ __device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> block_exclusive_pref
   __syncthreads();
 
   const Opt<A> tile_ex = sh.carry;
-  const Opt<A> warp_ex = warp > 0 ? sh.warp[warp - 1] : Opt<A>{A{}, false};
-  Opt<A> lane_ex = shfl_up_opt(incl, 1);
-  if (lane == 0) lane_ex.has = false;
-  return opt_combine(aop, opt_combine(aop, tile_ex, warp_ex), lane_ex);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int wi = r * NW + int(warp);
+    const Opt<A> warp_ex = wi > 0 ? sh.warp[wi - 1] : Opt<A>{A{}, false};
+    Opt<A> lane_ex = shfl_up_opt(incl[r], 1);
+    if (lane == 0) lane_ex.has = false;
+    ex[r] = opt_combine(aop, opt_combine(aop, tile_ex, warp_ex), lane_ex);
+  }
 }
 
 template <class T, int IT>
@@ -372,7 +392,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const ScanArgs<T, S,
   for (int k = 1; k < IT; ++k)
     if (k < count) last = regs[k];
 
-  const Opt<A> pre = block_exclusive_prefix(a, tile, s_epoch, Opt<A>{last, count > 0}, sh);
+  const Opt<A> tot1[1] = {Opt<A>{last, count > 0}};
+  Opt<A> pre1[1];
+  block_exclusive_prefix<1>(a, tile, s_epoch, tot1, sh, pre1);
+  const Opt<A> pre = pre1[0];
   if (count == 0) return;
 
   // compose outputs in registers and store once (:579-600)
@@ -413,23 +436,33 @@ constexpr uint32_t kSmemScanDyn = kSmemTileBytes + 1024;                 // + sw
 // `tmap_out` (used when tma_store) views dst as 128-byte rows; only for
 // sizeof(S) == sizeof(T), where each output chunk overwrites its input chunk
 // in shared memory and the finished tile leaves with one TMA tensor store.
-// Resident CTAs per SM the smem kernel is compiled for: 6 x 33 KB of tile
-// (Little's law) needs <= 40 registers; wide carries get 4.
-template <class S, class Op>
+//
+// R sub-tiles per CTA: the tile is R x 32 KB (R boxes of 256 rows); thread t
+// owns row t of every sub-tile.  R = 2 halves the number of tile states, of
+// look-back pollers and of the claim rate for the same bytes in flight (the
+// look-back's lag and its per-round latency both scale with them).
+//
+// Resident CTAs per SM the kernel is compiled for: 6 x 33 KB (R = 1) or
+// 3 x 65 KB (R = 2) of tile (Little's law) — <= 40 / 80
+// registers; wide carries get 2/3 of that.
+template <class S, class Op, int R>
 constexpr int scan_smem_min_blocks() {
-  return sizeof(typename ScanMath<S, Op>::C) <= 8 ? 6 : 4;
+  return (sizeof(typename ScanMath<S, Op>::C) <= 8 ? 6 : 4) / R;
 }
 
-template <class T, class S, class F, class Op, bool Inclusive>
-__global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op>())
+constexpr uint32_t scan_smem_dyn(int R) { return uint32_t(R) * kSmemTileBytes + 1024; }
+
+template <class T, class S, class F, class Op, bool Inclusive, int R>
+__global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>())
     scan_smem_kernel(const ScanArgs<T, S, F, Op> a, const __grid_constant__ CUtensorMap tmap,
                      const __grid_constant__ CUtensorMap tmap_out, bool tma_store) {
   using M = ScanMath<S, Op>;
   using A = typename M::A;
-  constexpr int IT = smem_scan_items<T>();  // items per thread (one 128-byte row)
+  constexpr int IT = smem_scan_items<T>();  // items per thread row (one 128-byte row)
   constexpr int EPC = 16 / int(sizeof(T));  // items per 16-byte chunk
   constexpr int NCH = kRowBytes / 16;       // chunks per row
-  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
+  constexpr uint64_t kSub = uint64_t(kScanThreads) * IT;  // items per sub-tile
+  constexpr uint64_t kTile = kSub * R;
   extern __shared__ unsigned char dyn_smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t s_tile, s_epoch, s_phase;
@@ -437,6 +470,12 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op>())
   auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
   unsigned char* tile_mem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
+  auto load_tile = [&](uint32_t t) {
+    mbar_arrive_expect_tx(&bar, uint32_t(R) * kSmemTileBytes);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      tma_load_2d(tile_mem + size_t(r) * kSmemTileBytes, &tmap, 0, (int(t) * R + r) * kScanThreads, &bar);
+  };
 
   if (threadIdx.x == 0) {
     // The tile to load is guessed as blockIdx.x and its TMA issued BEFORE the
@@ -446,10 +485,7 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op>())
     const bool gfull = uint64_t(g + 1) * kTile <= a.n;
     mbar_init(&bar, 1);
     fence_mbar_init();
-    if (gfull) {
-      mbar_arrive_expect_tx(&bar, kSmemTileBytes);
-      tma_load_2d(tile_mem, &tmap, 0, int(g) * kScanThreads, &bar);
-    }
+    if (gfull) load_tile(g);
     uint32_t e;
     const uint32_t t = claim_tile(a, e);
     s_tile = t;
@@ -458,8 +494,7 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op>())
     if (t != g) {
       if (gfull) mbar_wait(&bar, 0);  // drain the speculative copy
       if (uint64_t(t + 1) * kTile <= a.n) {
-        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
-        tma_load_2d(tile_mem, &tmap, 0, int(t) * kScanThreads, &bar);
+        load_tile(t);
         s_phase = gfull ? 1u : 0u;
       }
     }
@@ -473,101 +508,123 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op>())
     a.trace[tile * 8 + 5] = sm;
   }
   const bool full = (tile + 1) * kTile <= a.n;
-  const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * IT;
-  const uint64_t avail = base < a.n ? a.n - base : 0;
-  const int count = full ? IT : (avail >= uint64_t(IT) ? IT : int(avail));
+  uint64_t base[R];
+  int count[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    base[r] = tile * kTile + uint64_t(r) * kSub + uint64_t(threadIdx.x) * IT;
+    const uint64_t avail = base[r] < a.n ? a.n - base[r] : 0;
+    count[r] = full ? IT : (avail >= uint64_t(IT) ? IT : int(avail));
+  }
 
-  // ---- pass 1: ordered fold of this thread's row
-  Opt<A> tot{A{}, false};
+  // ---- pass 1: ordered fold of this thread's rows
+  Opt<A> tot[R];
   if (full) {
     mbar_wait(&bar, s_phase);
     trace_mark(a.trace, tile, 1);
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const uint4 v = lds128(tile_mem + swz128(threadIdx.x, c));
-      T x[EPC];
-      memcpy(x, &v, 16);
+    for (int r = 0; r < R; ++r) {
+      const unsigned char* tm = tile_mem + size_t(r) * kSmemTileBytes;
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) {
-        const A y = M::lift(a.f(x[e]));
-        tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
+      for (int c = 0; c < NCH; ++c) {
+        const uint4 v = lds128(tm + swz128(threadIdx.x, c));
+        T x[EPC];
+        memcpy(x, &v, 16);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const A y = M::lift(a.f(x[e]));
+          tot[r].v = (c == 0 && e == 0) ? y : aop(tot[r].v, y);
+        }
       }
+      tot[r].has = true;
     }
-    tot.has = true;
   } else {
-    for (int k = 0; k < count; ++k) {
-      const A y = M::lift(a.f(a.src[base + k]));
-      tot.v = k == 0 ? y : aop(tot.v, y);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      tot[r] = Opt<A>{A{}, false};
+      for (int k = 0; k < count[r]; ++k) {
+        const A y = M::lift(a.f(a.src[base[r] + k]));
+        tot[r].v = k == 0 ? y : aop(tot[r].v, y);
+      }
+      tot[r].has = count[r] > 0;
     }
-    tot.has = count > 0;
   }
 
   trace_mark(a.trace, tile, 2);
-  Opt<A> run = block_exclusive_prefix(a, tile, s_epoch, tot, sh);
+  Opt<A> run[R];
+  block_exclusive_prefix<R>(a, tile, s_epoch, tot, sh, run);
   trace_mark(a.trace, tile, 3);
-  if (count == 0) return;
 
   // ---- pass 2: running prefixes, stored as they are produced
   if (full) {
-    const bool vec = is_aligned(a.dst + base, 16);
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const uint4 v = lds128(tile_mem + swz128(threadIdx.x, c));
-      T x[EPC];
-      memcpy(x, &v, 16);
-      S o[EPC];
+    for (int r = 0; r < R; ++r) {
+      unsigned char* tm = tile_mem + size_t(r) * kSmemTileBytes;
+      const bool vec = is_aligned(a.dst + base[r], 16);
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) {
-        const A y = M::lift(a.f(x[e]));
-        if constexpr (Inclusive) {
-          run.v = run.has ? aop(run.v, y) : y;
-          run.has = true;
-          o[e] = M::lower(run.v);
+      for (int c = 0; c < NCH; ++c) {
+        const uint4 v = lds128(tm + swz128(threadIdx.x, c));
+        T x[EPC];
+        memcpy(x, &v, 16);
+        S o[EPC];
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const A y = M::lift(a.f(x[e]));
+          if constexpr (Inclusive) {
+            run[r].v = run[r].has ? aop(run[r].v, y) : y;
+            run[r].has = true;
+            o[e] = M::lower(run[r].v);
+          } else {
+            o[e] = run[r].has ? M::lower(run[r].v) : a.identity;
+            run[r].v = run[r].has ? aop(run[r].v, y) : y;
+            run[r].has = true;
+          }
+        }
+        if constexpr (sizeof(S) == sizeof(T)) {
+          if (tma_store) {
+            uint4 w;
+            memcpy(&w, o, 16);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(tm + swz128(threadIdx.x, c))),
+                         "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                         : "memory");
+            continue;
+          }
+        }
+        S* d = a.dst + base[r] + uint64_t(c) * EPC;
+        if (vec) {
+          store_items<S, EPC>(d, o);
         } else {
-          o[e] = run.has ? M::lower(run.v) : a.identity;
-          run.v = run.has ? aop(run.v, y) : y;
-          run.has = true;
-        }
-      }
-      if constexpr (sizeof(S) == sizeof(T)) {
-        if (tma_store) {
-          uint4 w;
-          memcpy(&w, o, 16);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(tile_mem + swz128(threadIdx.x, c))),
-                       "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
-                       : "memory");
-          continue;
-        }
-      }
-      S* d = a.dst + base + uint64_t(c) * EPC;
-      if (vec) {
-        store_items<S, EPC>(d, o);
-      } else {
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) d[e] = o[e];
+          for (int e = 0; e < EPC; ++e) d[e] = o[e];
+        }
       }
     }
     if (sizeof(S) == sizeof(T) && tma_store) {
       fence_proxy_async_smem();  // generic smem writes -> visible to the TMA engine
       __syncthreads();
       if (threadIdx.x == 0) {
-        tma_store_2d(&tmap_out, 0, int(tile) * kScanThreads, tile_mem);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          tma_store_2d(&tmap_out, 0, (int(tile) * R + r) * kScanThreads, tile_mem + size_t(r) * kSmemTileBytes);
         tma_store_commit();
         tma_store_wait_read();  // keep the CTA (and its smem) alive until read
       }
     }
     trace_mark(a.trace, tile, 4);
   } else {
-    for (int k = 0; k < count; ++k) {
-      const A y = M::lift(a.f(a.src[base + k]));
-      if constexpr (Inclusive) {
-        run.v = run.has ? aop(run.v, y) : y;
-        run.has = true;
-        a.dst[base + k] = M::lower(run.v);
-      } else {
-        a.dst[base + k] = run.has ? M::lower(run.v) : a.identity;
-        run.v = run.has ? aop(run.v, y) : y;
-        run.has = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      for (int k = 0; k < count[r]; ++k) {
+        const A y = M::lift(a.f(a.src[base[r] + k]));
+        if constexpr (Inclusive) {
+          run[r].v = run[r].has ? aop(run[r].v, y) : y;
+          run[r].has = true;
+          a.dst[base[r] + k] = M::lower(run[r].v);
+        } else {
+          a.dst[base[r] + k] = run[r].has ? M::lower(run[r].v) : a.identity;
+          run[r].v = run[r].has ? aop(run[r].v, y) : y;
+          run[r].has = true;
+        }
       }
     }
   }
@@ -970,6 +1027,10 @@ inline uint32_t scan_lookback_mode() {
   static const uint32_t v = scan_env_u32("FORGE_SCAN_LOOKBACK", 0);
   return v;
 }
+inline uint32_t scan_backoff_ns() {
+  static const uint32_t v = scan_env_u32("FORGE_SCAN_BACKOFF_NS", 0);
+  return v;
+}
 inline uint32_t scan_state_words_override() {
   static const uint32_t v = scan_env_u32("FORGE_SCAN_STATE_WORDS", 0);
   return v;
@@ -1123,21 +1184,34 @@ cudaError_t launch_scan_chain(const ScanArgs<T, S, F, Op>& a, const CUtensorMap&
   return cudaLaunchKernelEx(&cfg, kern, a, tmap, tmap_out, tstore, ns, lag);
 }
 
-template <class T, class S, class F, class Op, bool Inclusive>
-inline void scan_smem_prepare() {
+// 32 KB sub-tiles per CTA tile of the default kernel: measured (f32 / i32 /
+// affine / argmax / Mat2 at 2^28, GB/s) R=1: 4896 / 4941 / 3747 / 4612 / 3801,
+// R=2: 4635 / 4658 / 3491 / 4264 / 4532 — so R = 2 only for 16-byte elements.
+// (The R = 2 kernel is instantiated for those only; FORGE_SCAN_SUBTILES=1
+// forces R = 1 for them.)
+template <class T>
+inline int scan_subtiles() {
+  static const int v = int(scan_env_u32("FORGE_SCAN_SUBTILES", 0));
+  return sizeof(T) >= 16 && v != 1 ? 2 : 1;
+}
+
+template <class T, class S, class F, class Op, bool Inclusive, int R>
+cudaError_t launch_scan_smem(const ScanArgs<T, S, F, Op>& a, const CUtensorMap& tmap, const CUtensorMap& tmap_out,
+                             bool tstore, cudaStream_t stream) {
+  auto kern = scan_smem_kernel<T, S, F, Op, Inclusive, R>;
   static thread_local int done_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (done_dev != dev) {
-    cudaFuncSetAttribute(scan_smem_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kSmemScanDyn));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_smem_dyn(R)));
     // Maximum shared-memory carveout: residency (tiles in flight) is what
     // hides the look-back latency; the kernel barely uses L1.
-    cudaFuncSetAttribute(scan_smem_kernel<T, S, F, Op, Inclusive>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(scan_env_u32("FORGE_SCAN_CARVEOUT", 100)));
     done_dev = dev;
   }
+  kern<<<a.ntiles, kScanThreads, scan_smem_dyn(R), stream>>>(a, tmap, tmap_out, tstore);
+  return cudaGetLastError();
 }
 
 template <class T, class S, class F, class Op>
@@ -1150,7 +1224,8 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   ScanArgs<T, S, F, Op> a{src,      dst,      n,         src_stride, dst_stride,
                           f,        op,       identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
-                          static_cast<uint32_t*>(ws), 0u, WsT::kSlotWords, scan_lookback_mode(), nullptr};
+                          static_cast<uint32_t*>(ws), 0u, WsT::kSlotWords, scan_lookback_mode(), nullptr,
+                          scan_backoff_ns()};
   if (scan_env_u32("FORGE_SCAN_TRACE", 0))  // development: phase timestamps after the tile states
     a.trace = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + WsT::bytes(n));
   {
@@ -1169,6 +1244,9 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
     CUtensorMap tmap_out = tmap;
     const bool tstore = sizeof(S) == sizeof(T) && !scan_env_u32("FORGE_SCAN_NO_TMA_STORE", 0) &&
                         make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
+#ifdef FORGE_SCAN_EXPERIMENTS
+    // Measured alternatives, built only with
+    // `make EXPERIMENTS=1`: FORGE_SCAN_PATH=chain|ws|pipe, FORGE_SCAN_CLUSTER=K.
     if (scan_path() == 3) {
       const cudaError_t e = inclusive ? launch_scan_chain<T, S, F, Op, true>(a, tmap, tmap_out, tstore, stream)
                                       : launch_scan_chain<T, S, F, Op, false>(a, tmap, tmap_out, tstore, stream);
@@ -1205,14 +1283,16 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
       }
       return cudaGetLastError();
     }
-    if (inclusive) {
-      scan_smem_prepare<T, S, F, Op, true>();
-      scan_smem_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap, tmap_out, tstore);
-    } else {
-      scan_smem_prepare<T, S, F, Op, false>();
-      scan_smem_kernel<T, S, F, Op, false><<<a.ntiles, kScanThreads, kSmemScanDyn, stream>>>(a, tmap, tmap_out, tstore);
+#endif
+    if constexpr (sizeof(T) >= 16) {
+      if (scan_subtiles<T>() == 2) {
+        a.ntiles = uint32_t(ceil_div(n, 2 * WsT::kTileSmem));
+        return inclusive ? launch_scan_smem<T, S, F, Op, true, 2>(a, tmap, tmap_out, tstore, stream)
+                         : launch_scan_smem<T, S, F, Op, false, 2>(a, tmap, tmap_out, tstore, stream);
+      }
     }
-    return cudaGetLastError();
+    return inclusive ? launch_scan_smem<T, S, F, Op, true, 1>(a, tmap, tmap_out, tstore, stream)
+                     : launch_scan_smem<T, S, F, Op, false, 1>(a, tmap, tmap_out, tstore, stream);
   }
   }
   a.ntiles = uint32_t(ceil_div(n, WsT::kTileGeneral));

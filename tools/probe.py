@@ -52,3 +52,21 @@ if what == "mapreduce":
             out[name + "_ok"] = bool(orc.within(op, got, ex, sc, 1e-5)[0]) if orc.ncomp(op) else bool(got[0] == want)
         del src
     print(json.dumps({"mapreduce": out}))
+if what == "matrix":
+    nn = 16384
+    op = capi.MV_F32_PLUS_TIMES
+    A = dev.empty(op, nn * nn); dev.fill_synthetic(op, A, nn * nn, 5)
+    x = dev.empty(op, nn); dev.fill_synthetic(op, x, nn, 6)
+    y = dev.empty(op, nn, "S")
+    byts = nn * nn * 4 + 2 * nn * 4
+    out["gevm"] = round(byts / t(lambda: dev.matvec(op, A, nn, nn, x, y, ws)) / 1e6, 1)
+    out["gemv"] = round(byts / t(lambda: dev.vecmat(op, A, nn, nn, x, y, ws)) / 1e6, 1)
+    o16 = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    out["mapreduce_1GiB"] = round(nn * nn * 4 / t(lambda: dev.mapreduce(capi.F32_SUMSQ, A, nn * nn, o16, ws)) / 1e6, 1)
+    print(json.dumps({"matrix": out}))
+if what == "copy":
+    nb = 2 << 30
+    a = torch.empty(nb, dtype=torch.uint8, device="cuda"); b = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    out["forge_copy"] = round(2 * nb / t(lambda: dev.copy(a, b, nb)) / 1e6, 1)
+    out["torch_copy"] = round(2 * nb / t(lambda: b.copy_(a)) / 1e6, 1)
+    print(json.dumps({"copy": out}))

@@ -9,7 +9,7 @@ op = int(sys.argv[1]) if len(sys.argv) > 1 else capi.F32_SUM
 n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 28)
 ws = dev.Workspace()
 need = dev.workspace_bytes(capi.PRIM_SCAN, op, n)
-tiles = n // 8192 + 2
+tiles = n // 8192 + 2  # upper bound for any sub-tile count
 ws.ensure(need + tiles * 64 + 4096)
 src = dev.empty(op, n); dev.fill_synthetic(op, src, n, 3); dst = dev.empty(op, n, "S")
 for _ in range(3):
