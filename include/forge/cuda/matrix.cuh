@@ -156,6 +156,88 @@ __global__ void __launch_bounds__(kMatThreads) gevm_kernel(const GevmArgs<T, S, 
   }
 }
 
+// Column-group variant for commutative ops on aligned data (the common case):
+// a warp owns CPW adjacent columns and a row split; every step a lane loads
+// its 32 bytes of x ONCE and 32 bytes of each of the CPW columns, so x costs
+// one load per CPW columns and the registers a warp keeps in flight are almost
+// all A (the one-column kernel holds as much x as A in flight, 100 registers,
+// 2 CTAs/SM).  Split partials are folded in split order by the last split of
+// the group (ticket of its first column).
+template <class T, class S, class F2, class Op, bool UsesX, int CPW>
+__global__ void __launch_bounds__(kMatThreads) gevm_cols_kernel(const GevmArgs<T, S, F2, Op> a) {
+  constexpr int VE = mr_vec_elems<T>();
+  __shared__ bool s_last[kMatWarps];
+  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
+  const uint64_t groups = ceil_div(a.p, CPW);
+  const uint64_t item = uint64_t(blockIdx.x) * kMatWarps + warp;
+  if (item >= groups * a.ks) return;
+  const uint64_t grp = item / a.ks;
+  const uint32_t s = uint32_t(item % a.ks);
+  const uint64_t j0 = grp * CPW;
+  const int nc = a.p - j0 < uint64_t(CPW) ? int(a.p - j0) : CPW;
+  const uint64_t r0 = uint64_t(s) * a.rows_per_split;
+  const uint64_t r1 = r0 + a.rows_per_split < a.n ? r0 + a.rows_per_split : a.n;
+  const T xz{};
+  auto fx = [&](const T& xv, const T& av) { return a.f(UsesX ? xv : xz, av); };
+
+  S acc[CPW];
+  bool has = false;
+  const uint64_t nv = (r1 - r0) / VE;  // r0 is a multiple of 32 * VE
+  for (uint64_t k = lane; k < nv; k += kWarp) {
+    const uint64_t i = r0 + k * VE;
+    T xx[VE], av[CPW][VE];
+    if constexpr (UsesX) load_items<T, VE, false>(a.x + i, xx);
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+      if (c < nc) load_items<T, VE>(a.A + (j0 + c) * a.n + i, av[c]);
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        const S t = fx(UsesX ? xx[e] : xz, av[c][e]);
+        acc[c] = (has || e > 0) ? a.op(acc[c], t) : t;
+      }
+    }
+    has = true;
+  }
+  Opt<S> part[CPW];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) part[c] = Opt<S>{acc[c], has};
+  for (uint64_t i = r0 + nv * VE + lane; i < r1; i += kWarp) {
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+      if (c < nc) part[c] = opt_combine(a.op, part[c], Opt<S>{fx(UsesX ? a.x[i] : xz, a.A[(j0 + c) * a.n + i]), true});
+  }
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) part[c] = warp_allreduce_comm(a.op, part[c]);
+
+  if (a.ks == 1) {
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < CPW; ++c)
+        if (c < nc) a.y[j0 + c] = part[c].v;
+    }
+    return;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+      if (c < nc) a.partials[(j0 + c) * a.ks + s] = part[c].v;
+    const uint32_t t = atom_add_acq_rel_gpu(a.tickets + j0, 1u);
+    s_last[warp] = (t == a.ks - 1);
+    if (s_last[warp]) st_relaxed_gpu(a.tickets + j0, 0u);
+  }
+  __syncwarp();
+  if (!s_last[warp]) return;
+  // lane c < nc folds column j0 + c in split order
+  if (int(lane) < nc) {
+    const S* pp = a.partials + (j0 + lane) * a.ks;
+    S v = ld_strong(pp);
+    for (uint32_t q = 1; q < a.ks; ++q) v = a.op(v, ld_strong(pp + q));
+    a.y[j0 + lane] = v;
+  }
+}
+
 template <class T, class S, class F2, class Op>
 struct GemvArgs {
   const T* A;
@@ -369,11 +451,41 @@ inline GemvPlan plan_gemv(uint64_t n, uint64_t p) {
   return GemvPlan{uint32_t(ks), cps, uint32_t(row_blocks), row_blocks * ks};
 }
 
+constexpr int kGevmCols = 4;  // columns per warp of gevm_cols_kernel
+
+inline bool gevm_cols_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("FORGE_GEVM_COLS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// Plan of gevm_cols_kernel: enough (column group, row split) warps for ~14
+// CTAs per SM so the last wave is nearly full.
+template <class T>
+inline GevmPlan plan_gevm_cols(uint64_t n, uint64_t p) {
+  constexpr int VE = mr_vec_elems<T>();
+  const uint64_t groups = ceil_div(p, kGevmCols);
+  const uint64_t target = uint64_t(device_props().sm_count) * kMatWarps * 14;
+  uint64_t ks = groups >= target ? 1 : ceil_div(target, groups);
+  const uint64_t gran = uint64_t(kWarp) * VE;
+  const uint64_t max_ks = ceil_div(n, gran * 8);  // >= 8 steps per split
+  if (ks > max_ks) ks = max_ks;
+  if (ks < 1) ks = 1;
+  if (ks > 4096) ks = 4096;
+  uint64_t rps = round_up(ceil_div(n, ks), gran);
+  ks = ceil_div(n, rps);
+  if (ks < 1) ks = 1;
+  return GevmPlan{uint32_t(ks), rps, ceil_div(groups * ks, kMatWarps)};
+}
+
 template <class T, class S>
 inline uint64_t gevm_ws_bytes(uint64_t n, uint64_t p) {
-  GevmPlan pl = plan_gevm<T>(n, p);
-  if (pl.ks == 1) return 256;
-  return 256 + round_up(p * sizeof(uint32_t), 256) + p * pl.ks * sizeof(S);
+  const GevmPlan pl = plan_gevm<T>(n, p), pc = plan_gevm_cols<T>(n, p);
+  const uint64_t ks = pl.ks > pc.ks ? pl.ks : pc.ks;
+  if (ks == 1) return 256;
+  return 256 + round_up(p * sizeof(uint32_t), 256) + p * ks * sizeof(S);
 }
 
 template <class T, class S>
@@ -388,13 +500,20 @@ cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, co
                         const Op& op, void* ws, cudaStream_t stream) {
   if (p == 0 || n == 0) return cudaSuccess;
   constexpr int VE = mr_vec_elems<T>();
-  GevmPlan pl = plan_gevm<T>(n, p);
-  GevmArgs<T, S, F2, Op> a{A, x, y, n, p, f, op, pl.ks, pl.rows_per_split, false, nullptr, nullptr};
-  a.vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && (!UsesX || is_aligned(x, 32));
+  const bool vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && (!UsesX || is_aligned(x, 32));
+  const bool cols = !Ordered && vec && gevm_cols_enabled();
+  GevmPlan pl = cols ? plan_gevm_cols<T>(n, p) : plan_gevm<T>(n, p);
+  GevmArgs<T, S, F2, Op> a{A, x, y, n, p, f, op, pl.ks, pl.rows_per_split, vec, nullptr, nullptr};
   if (pl.ks > 1) {
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);
     a.partials = reinterpret_cast<S*>(w + round_up(p * sizeof(uint32_t), 256));
+  }
+  if constexpr (!Ordered) {
+    if (cols) {
+      gevm_cols_kernel<T, S, F2, Op, UsesX, kGevmCols><<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
+      return cudaGetLastError();
+    }
   }
   gevm_kernel<T, S, F2, Op, UsesX, Ordered><<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
   return cudaGetLastError();

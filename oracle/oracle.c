@@ -533,9 +533,35 @@ int orc_mapreduce(forge_op op, const void* src, uint64_t n, uint64_t stride, voi
   return 0;
 }
 
+/* Synthetic f32 inputs are integers times 2^-24 (gen_f32_sym / gen_f32_pos),
+ * so their sums — and sums of |x| — are EXACT in int64 units of 2^-24 for any
+ * n <= 2^38: the f32-sum oracle streams at integer speed (the long-double fold
+ * costs ~60 ns per element; the 2^33-element BASELINE C5 size needs this). */
+static int f32_sum_grid(forge_op op) { return op == FORGE_OP_F32_SUM; }
+static int64_t f32_units(uint64_t u, int32_t variant) {
+  const float v = variant == 1 ? gen_f32_pos(u) : gen_f32_sym(u);
+  return (int64_t)llrintf(v * 16777216.0f); /* exact: |v| <= 1, 24-bit grid */
+}
+
 int orc_mapreduce_synthetic(forge_op op, uint64_t n, uint64_t seed, int32_t variant, void* out_S,
                             double* exact, double* scale) {
   unsigned char t[16];
+  if (f32_sum_grid(op) && n > 0) {
+    int64_t acc = 0, abs_acc = 0;
+    /* integer sums are exact in any order: host threads may split the stream */
+#pragma omp parallel for reduction(+ : acc, abs_acc) schedule(static)
+    for (uint64_t i = 0; i < n; ++i) {
+      const int64_t k = f32_units(orc_mix(seed ^ i), variant);
+      acc += k;
+      abs_acc += k < 0 ? -k : k;
+    }
+    const long double ex = (long double)acc / 16777216.0L;
+    const float r = (float)ex;
+    memcpy(out_S, &r, 4);
+    if (exact) exact[0] = (double)ex;
+    if (scale) scale[0] = (double)((long double)abs_acc / 16777216.0L);
+    return 0;
+  }
   if (orc_float_components(op)) {
     facc acc;
     if (n == 0) facc_identity(op, &acc);
@@ -606,8 +632,13 @@ int orc_scan(forge_op op, int32_t inclusive, const void* src, uint64_t n, const 
   return 0;
 }
 
-int64_t orc_check_scan_synthetic(forge_op op, int32_t inclusive, uint64_t n, uint64_t seed,
-                                 int32_t variant, const void* got_S, double tol,
+/* Streaming scan check.  idx == NULL: every output got_S[i], i < n.  Else the
+ * outputs at the ascending positions idx[0..count) (got_S[k] is the output at
+ * idx[k]); the stream stops after the last sampled position — how the
+ * BASELINE C5 size (2^33 elements, 32 GiB of outputs) is checked without
+ * copying the outputs to the host. */
+static int64_t check_scan_stream(forge_op op, int32_t inclusive, uint64_t n, uint64_t seed, int32_t variant,
+                                 const uint64_t* idx, uint64_t count, const void* got_S, double tol,
                                  double* max_err) {
   const unsigned char* g = (const unsigned char*)got_S;
   uint32_t ss = s_size_of(op);
@@ -615,52 +646,163 @@ int64_t orc_check_scan_synthetic(forge_op op, int32_t inclusive, uint64_t n, uin
   unsigned char t[16];
   int64_t bad = 0;
   double worst = 0.0;
-  if (nc) {
+  uint64_t k = 0; /* next sample */
+  const uint64_t end = idx ? (count ? idx[count - 1] + 1 : 0) : n;
+  if (f32_sum_grid(op) && idx && count > 0) {
+    /* Sampled check, exact integer prefix: chunk sums in parallel, exclusive
+     * prefix over chunks, then every chunk checks its own samples. */
+    enum { NCHUNK = 256 };
+    static int64_t csum[NCHUNK + 1], cabs[NCHUNK + 1];
+    const uint64_t per = (end + NCHUNK - 1) / NCHUNK;
+#pragma omp parallel for schedule(dynamic)
+    for (int c = 0; c < NCHUNK; ++c) {
+      int64_t a = 0, b = 0;
+      const uint64_t lo = (uint64_t)c * per, hi = lo + per < end ? lo + per : end;
+      for (uint64_t i = lo; i < hi; ++i) {
+        const int64_t kk = f32_units(orc_mix(seed ^ i), variant);
+        a += kk;
+        b += kk < 0 ? -kk : kk;
+      }
+      csum[c + 1] = a;
+      cabs[c + 1] = b;
+    }
+    csum[0] = cabs[0] = 0;
+    for (int c = 0; c < NCHUNK; ++c) {
+      csum[c + 1] += csum[c];
+      cabs[c + 1] += cabs[c];
+    }
+    int64_t nbad = 0;
+    double w = 0.0;
+#pragma omp parallel for schedule(dynamic) reduction(+ : nbad)
+    for (int c = 0; c < NCHUNK; ++c) {
+      const uint64_t lo = (uint64_t)c * per, hi = lo + per < end ? lo + per : end;
+      uint64_t s0 = 0; /* first sample >= lo */
+      { uint64_t L = 0, R = count; while (L < R) { uint64_t M = (L + R) / 2; if (idx[M] < lo) L = M + 1; else R = M; } s0 = L; }
+      if (s0 >= count || idx[s0] >= hi) continue;
+      int64_t a = csum[c], b = cabs[c];
+      double lw = 0.0;
+      uint64_t kk2 = s0;
+      for (uint64_t i = lo; i < hi && kk2 < count; ++i) {
+        const int64_t ex_a = a, ex_b = b;
+        const int64_t u = f32_units(orc_mix(seed ^ i), variant);
+        a += u;
+        b += u < 0 ? -u : u;
+        while (kk2 < count && idx[kk2] == i) {
+          float gf;
+          memcpy(&gf, g + kk2 * ss, 4);
+          const int64_t ea = inclusive ? a : ex_a, eb = inclusive ? b : ex_b;
+          const double ex = (double)((long double)ea / 16777216.0L);
+          const double sc = (double)((long double)eb / 16777216.0L);
+          const double err = fabs((double)gf - ex);
+          const double rel = sc > 0 ? err / sc : (err > 0 ? INFINITY : 0.0);
+          if (rel > lw || rel != rel) lw = rel != rel ? INFINITY : rel;
+          if (!(err <= tol * sc)) ++nbad;
+          ++kk2;
+        }
+      }
+#pragma omp critical
+      if (lw > w) w = lw;
+    }
+    bad = nbad;
+    worst = w;
+  } else if (f32_sum_grid(op)) {
+    int64_t acc = 0, abs_acc = 0;
+    int has = 0;
+    for (uint64_t i = 0; i < end; ++i) {
+      const int64_t kk = f32_units(orc_mix(seed ^ i), variant);
+      const int64_t ex_acc = acc, ex_abs = abs_acc;
+      const int ex_has = has;
+      acc += kk;
+      abs_acc += kk < 0 ? -kk : kk;
+      has = 1;
+      while (!idx || (k < count && idx[k] == i)) {
+        float gf;
+        memcpy(&gf, g + (idx ? k : i) * ss, 4);
+        double ex, sc;
+        if (inclusive) {
+          ex = (double)((long double)acc / 16777216.0L);
+          sc = (double)((long double)abs_acc / 16777216.0L);
+        } else if (ex_has) {
+          ex = (double)((long double)ex_acc / 16777216.0L);
+          sc = (double)((long double)ex_abs / 16777216.0L);
+        } else {
+          ex = 0.0; /* identity */
+          sc = 0.0;
+        }
+        const double err = fabs((double)gf - ex);
+        const double rel = sc > 0 ? err / sc : (err > 0 ? INFINITY : 0.0);
+        if (rel > worst || rel != rel) worst = rel != rel ? INFINITY : rel;
+        if (!(err <= tol * sc)) ++bad;
+        if (!idx) break;
+        ++k;
+      }
+    }
+  } else if (nc) {
     facc acc, ident;
     facc_identity(op, &ident);
     memset(&acc, 0, sizeof acc);
-    for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t i = 0; i < end; ++i) {
       gen_one(op, orc_mix(seed ^ i), i, variant, t);
       long double v[4] = {0, 0, 0, 0}, s[4] = {0, 0, 0, 0};
       map_float(op, t, v, s);
       if (inclusive) fold_float(op, &acc, v, s);
-      const facc* cur = acc.has ? &acc : &ident;
-      for (int k = 0; k < nc; ++k) {
-        double got;
-        if (op == FORGE_OP_F64_SUM) {
-          memcpy(&got, g + i * ss, 8);
-        } else {
-          float gf;
-          memcpy(&gf, g + i * ss + 4 * k, 4);
-          got = gf;
+      while (!idx || (k < count && idx[k] == i)) {
+        const unsigned char* gi = g + (idx ? k : i) * ss;
+        const facc* cur = acc.has ? &acc : &ident;
+        for (int c = 0; c < nc; ++c) {
+          double got;
+          if (op == FORGE_OP_F64_SUM) {
+            memcpy(&got, gi, 8);
+          } else {
+            float gf;
+            memcpy(&gf, gi + 4 * c, 4);
+            got = gf;
+          }
+          double ex = (double)cur->v[c], sc = (double)cur->s[c];
+          double err = fabs(got - ex);
+          double rel = sc > 0 ? err / sc : (err > 0 ? INFINITY : 0.0);
+          if (rel > worst || rel != rel) worst = rel != rel ? INFINITY : rel;
+          if (!(err <= tol * sc)) {
+            ++bad;
+            break;
+          }
         }
-        double ex = (double)cur->v[k], sc = (double)cur->s[k];
-        double err = fabs(got - ex);
-        double rel = sc > 0 ? err / sc : (err > 0 ? INFINITY : 0.0);
-        if (rel > worst || rel != rel) worst = rel != rel ? INFINITY : rel;
-        if (!(err <= tol * sc)) {
-          ++bad;
-          break;
-        }
+        if (!idx) break;
+        ++k;
       }
       if (!inclusive) fold_float(op, &acc, v, s);
     }
   } else {
     sval acc = identity_of(op), ident = identity_of(op);
     int has = 0;
-    for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t i = 0; i < end; ++i) {
       gen_one(op, orc_mix(seed ^ i), i, variant, t);
       sval v = map_exact(op, t);
-      if (!inclusive) {
-        if (memcmp(g + i * ss, (has ? acc : ident).raw, ss) != 0) ++bad;
-      }
+      sval ex_before = has ? acc : ident;
       acc = has ? combine_exact(op, acc, v) : v;
       has = 1;
-      if (inclusive && memcmp(g + i * ss, acc.raw, ss) != 0) ++bad;
+      while (!idx || (k < count && idx[k] == i)) {
+        const unsigned char* gi = g + (idx ? k : i) * ss;
+        if (memcmp(gi, inclusive ? acc.raw : ex_before.raw, ss) != 0) ++bad;
+        if (!idx) break;
+        ++k;
+      }
     }
   }
   if (max_err) *max_err = worst;
   return bad;
+}
+
+int64_t orc_check_scan_synthetic(forge_op op, int32_t inclusive, uint64_t n, uint64_t seed,
+                                 int32_t variant, const void* got_S, double tol,
+                                 double* max_err) {
+  return check_scan_stream(op, inclusive, n, seed, variant, NULL, 0, got_S, tol, max_err);
+}
+
+int64_t orc_check_scan_synthetic_at(forge_op op, int32_t inclusive, uint64_t seed, int32_t variant,
+                                    const uint64_t* idx, uint64_t count, const void* got_at, double tol,
+                                    double* max_err) {
+  return check_scan_stream(op, inclusive, 0, seed, variant, idx, count, got_at, tol, max_err);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -76,6 +76,11 @@ int orc_mapreduce_synthetic(forge_op op, uint64_t n, uint64_t seed, int32_t vari
  * err/scale seen. */
 int64_t orc_check_scan_synthetic(forge_op op, int32_t inclusive, uint64_t n, uint64_t seed,
                                  int32_t variant, const void* got_S, double tol, double* max_err);
+/* Same check at ascending sampled positions idx[0..count): got_at[k] is the
+ * output at idx[k] (streams up to the last position). */
+int64_t orc_check_scan_synthetic_at(forge_op op, int32_t inclusive, uint64_t seed, int32_t variant,
+                                    const uint64_t* idx, uint64_t count, const void* got_at, double tol,
+                                    double* max_err);
 
 /* UnitFloat8 (algebra.hpp:15-28). */
 float orc_uf8_decode(uint8_t code);

@@ -26,7 +26,8 @@ def build_oracle(force: bool = False) -> Path:
     if force or not ORACLE_SO.exists() or ORACLE_SO.stat().st_mtime < max(
             src.stat().st_mtime, (HERE / "oracle.h").stat().st_mtime):
         ORACLE_SO.parent.mkdir(exist_ok=True)
-        subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-o", str(ORACLE_SO), str(src), "-lm"],
+        subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-fopenmp", "-o", str(ORACLE_SO), str(src),
+                        "-lm"],
                        check=True)
     return ORACLE_SO
 
@@ -51,6 +52,9 @@ def lib() -> C.CDLL:
         L.orc_vecmat.argtypes = [C.c_int, _P, _u64, _u64, _P, _P, _P, _P]
         L.orc_vload_pattern.argtypes = [_u64, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.orc_mapreduce_synthetic.argtypes = [C.c_int, _u64, _u64, C.c_int32, _P, _P, _P]
+        L.orc_check_scan_synthetic_at.restype = C.c_int64
+        L.orc_check_scan_synthetic_at.argtypes = [C.c_int, C.c_int32, _u64, C.c_int32, _P, _u64, _P, C.c_double,
+                                                  C.POINTER(C.c_double)]
         L.orc_check_scan_synthetic.restype = C.c_int64
         L.orc_check_scan_synthetic.argtypes = [C.c_int, C.c_int32, _u64, _u64, C.c_int32, _P, C.c_double,
                                                C.POINTER(C.c_double)]
@@ -191,6 +195,17 @@ def check_scan_synthetic(op, inclusive, n, seed, got: np.ndarray, tol: float, va
     worst = C.c_double()
     bad = lib().orc_check_scan_synthetic(op, 1 if inclusive else 0, n, seed, variant, _ptr(got), tol,
                                          C.byref(worst))
+    return int(bad), worst.value
+
+
+def check_scan_synthetic_at(op, inclusive, seed, idx: np.ndarray, got_at: np.ndarray, tol: float, variant=0):
+    """Streaming check of scan outputs at ascending positions `idx` only."""
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    assert np.all(np.diff(idx.astype(np.int64)) > 0), "positions must be strictly ascending"
+    got_at = _c(got_at)
+    worst = C.c_double()
+    bad = lib().orc_check_scan_synthetic_at(op, 1 if inclusive else 0, seed, variant, _ptr(idx), len(idx),
+                                            _ptr(got_at), tol, C.byref(worst))
     return int(bad), worst.value
 
 

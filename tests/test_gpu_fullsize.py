@@ -134,3 +134,52 @@ def test_uf8_decode_exhaustive_bitwise():
         got = m.read(d, 1, np.float32)[0]
         assert np.float32(got) == np.float32(L.orc_uf8_decode(c)), c
     m.close()
+
+
+def test_c5_sharded_scan_and_mapreduce_2pow33():
+    # BASELINE C5 at G = 1 box-local shards: n = 2^33 f32 (32 GiB in, 32 GiB out),
+    # exclusive scan and mapreduce through the multi-GPU exchange code path
+    # (order-preserving shard totals -> rank-order fold -> carry-seeded scans),
+    # G = 4 shards emulated on one GPU.  Outputs are checked by the streaming
+    # oracle at 4096 random positions plus every shard boundary +-1 (the
+    # outputs never leave the device in full).
+    op, n, G = capi.F32_SUM, 1 << 33, 4
+    seed = 0x5EED0C05
+    sz = 4
+    x = dev.empty(op, n)
+    dev.fill_synthetic(op, x, n, seed)
+    ws = dev.Workspace()
+    bounds = [n * g // G for g in range(G + 1)]
+    totals = torch.zeros(G * sz, dtype=torch.uint8, device="cuda")
+    parts = torch.zeros(G * sz, dtype=torch.uint8, device="cuda")
+    for g in range(G):
+        lo, hi = bounds[g], bounds[g + 1]
+        dev.reduce_ordered(op, x.data_ptr() + lo * sz, hi - lo, totals.data_ptr() + g * sz, ws)
+        dev.mapreduce(op, x.data_ptr() + lo * sz, hi - lo, parts.data_ptr() + g * sz, ws)
+    total = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    dev.fold(op, parts, G, total)
+    y = dev.empty(op, n, "S")
+    carry = torch.zeros(sz, dtype=torch.uint8, device="cuda")
+    has = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for g in range(G):
+        lo, hi = bounds[g], bounds[g + 1]
+        dev.fold(op, totals, G, carry, exclusive_upto=g, has_out=has)
+        torch.cuda.synchronize()
+        cin = carry if int(has.item()) else None
+        dev.scan(op, False, x.data_ptr() + lo * sz, y.data_ptr() + lo * sz, hi - lo, ws, carry_in=cin)
+    torch.cuda.synchronize()
+    del x
+    rng = np.random.default_rng(5)
+    idx = set(int(v) for v in rng.integers(0, n, size=4096))
+    for b in bounds[1:-1]:
+        idx.update((b - 1, b, b + 1))
+    idx.update((0, 1, n - 1))
+    idx = np.array(sorted(idx), dtype=np.int64)
+    got_at = y.view(torch.float32)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    del y
+    bad, worst = orc.check_scan_synthetic_at(op, False, seed, idx.astype(np.uint64), got_at, TOL[op])
+    assert bad == 0, f"{bad} of {len(idx)} sampled outputs off, worst err/scale {worst:.3e}"
+    got = to_np(total[:4], np.float32)
+    _, ex, sc = orc.mapreduce_synthetic(op, n, seed)
+    ok, rel = orc.within(op, got, ex, sc, TOL[op])
+    assert ok, rel

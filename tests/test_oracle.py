@@ -195,3 +195,22 @@ def test_oracle_vs_live_reference_both_backends(op):
     for backend in (orc.SIM, orc.THREADS):
         y, _ = orc.ref_scan(op, True, x, backend=backend, seed=5)
         same(op, d, y.view(np.uint8), ex, sc, f"live scan backend={backend}")
+
+
+@pytest.mark.parametrize("op", [0, 5, 10, 11, 12])
+@pytest.mark.parametrize("inclusive", [True, False])
+def test_check_scan_synthetic_at_matches_full_check(op, inclusive):
+    """The sampled streaming check (used for the 2^33 C5 size) agrees with the
+    oracle's own scan: clean samples pass, one corrupted sample is caught."""
+    n, seed = 20_011, 0x5EED0C06
+    x = orc.fill(op, n, seed)
+    want, _, _ = orc.scan(op, inclusive, x)
+    idx = np.array(sorted({0, 1, 2, 4095, 4096, 9999, n - 1}), dtype=np.uint64)
+    got_at = want[idx.astype(np.int64)].copy()
+    bad, _ = orc.check_scan_synthetic_at(op, inclusive, seed, idx, got_at, 1e-5)
+    assert bad == 0
+    raw = got_at.view(np.uint8).copy()
+    k = 3 * got_at.dtype.itemsize
+    raw[k:k + 4] ^= np.frombuffer(np.float32(1.5).tobytes(), np.uint8)
+    bad, _ = orc.check_scan_synthetic_at(op, inclusive, seed, idx, raw.view(got_at.dtype), 1e-5)
+    assert bad == 1

@@ -1,4 +1,4 @@
-"""Runs one primitive a few times (for ncu captures). usage: one_kernel.py mapreduce|scan|gevm|gemv [op]"""
+"""Runs one primitive a few times (for ncu captures). usage: one_kernel.py mapreduce|scan|gevm|gemv|copy [op]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,6 +16,10 @@ elif what == "scan":
     n = 1 << 28
     x = dev.empty(op, n); dev.fill_synthetic(op, x, n, 1); y = dev.empty(op, n, "S")
     for _ in range(3): dev.scan(op, True, x, y, n, ws)
+elif what == "copy":
+    nb = 2 << 30
+    a = torch.empty(nb, dtype=torch.uint8, device="cuda"); b = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    for _ in range(3): dev.copy(a, b, nb)
 else:
     op = int(sys.argv[2]) if len(sys.argv) > 2 else capi.MV_F32_PLUS_TIMES
     nn = 16384
