@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(kMatThreads) gevm_kernel(const GevmArgs<T, S, 
 // all A (the one-column kernel holds as much x as A in flight, 100 registers,
 // 2 CTAs/SM).  Split partials are folded in split order by the last split of
 // the group (ticket of its first column).
-template <class T, class S, class F2, class Op, bool UsesX, int CPW>
-__global__ void __launch_bounds__(kMatThreads) gevm_cols_kernel(const GevmArgs<T, S, F2, Op> a) {
+template <class T, class S, class F2, class Op, bool UsesX, int CPW, int MINB = 1>
+__global__ void __launch_bounds__(kMatThreads, MINB) gevm_cols_kernel(const GevmArgs<T, S, F2, Op> a) {
   constexpr int VE = mr_vec_elems<T>();
   __shared__ bool s_last[kMatWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
@@ -251,7 +251,10 @@ struct GemvArgs {
   uint32_t row_blocks;
   bool vec;
   S* partials;        // [ks][n]
-  uint32_t* tickets;  // [row_blocks]
+  uint32_t* tickets;  // [row_blocks][groups + 1]
+  uint32_t gsize;     // splits per fold group
+  uint32_t groups;    // fold groups (1 = one flat fold)
+  S* gpartials;       // [groups][n] when groups > 1
 };
 
 template <class T>
@@ -330,72 +333,96 @@ __global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, 
     }
     return;
   }
-  // Partials [s][row]; last block of this row-block folds in split order.
+  // Partials [s][row], folded in split order in two levels so the fold tail
+  // is ~2*sqrt(ks) partial rows instead of ks: the last split of each group of
+  // `gsize` splits folds the group into a group partial, the last group folds
+  // the group partials.  (One CTA's memory parallelism bounds a fold — 4
+  // partial rows in flight per thread — and the flat fold of 56 splits was the
+  // kernel's tail.)
   if (i0 < a.n) {
 #pragma unroll
     for (int e = 0; e < VE; ++e)
       if (i0 + e < a.n) a.partials[uint64_t(s) * a.n + i0 + e] = acc[e];
   }
+  const uint32_t grp = s / a.gsize;
+  const uint32_t q0 = grp * a.gsize, q1 = q0 + a.gsize < a.ks ? q0 + a.gsize : a.ks;
+  uint32_t* tk = a.tickets + uint64_t(rb) * (a.groups + 1);
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t t = atom_add_acq_rel_gpu(a.tickets + rb, 1u);
-    s_last = (t == a.ks - 1);
-    if (s_last) st_relaxed_gpu(a.tickets + rb, 0u);
+    const uint32_t t = atom_add_acq_rel_gpu(tk + grp, 1u);
+    s_last = (t == q1 - q0 - 1);
+    if (s_last) st_relaxed_gpu(tk + grp, 0u);
   }
   __syncthreads();
   if (!s_last) return;
-  // Fold the split partials of this thread's rows in split order.  Full row
-  // groups read each split's VE partials with coalesced strong vector loads,
-  // four splits in flight.
-  if (i0 + VE <= a.n && (sizeof(S) * VE) % 16 == 0 && is_aligned(a.partials + i0, 16) &&
-      (uint64_t(a.n) * sizeof(S)) % 16 == 0) {
-    constexpr int W = int(sizeof(S) * VE) / 16;  // 16-byte words per row group
-    auto load_group = [&](uint32_t q, S (&dst)[VE]) {
-      uint4 w[W];
-      const uint4* p = reinterpret_cast<const uint4*>(a.partials + uint64_t(q) * a.n + i0);
+
+  // Ordered fold of `count` partial rows (stride n) for this thread's rows.
+  auto fold_rows = [&](const S* base, uint32_t count, S* out) {
+    if (i0 + VE <= a.n && (sizeof(S) * VE) % 16 == 0 && is_aligned(base + i0, 16) &&
+        (uint64_t(a.n) * sizeof(S)) % 16 == 0) {
+      constexpr int W = int(sizeof(S) * VE) / 16;  // 16-byte words per row group
+      auto load_group = [&](uint32_t q, S (&dst)[VE]) {
+        uint4 w[W];
+        const uint4* p = reinterpret_cast<const uint4*>(base + uint64_t(q) * a.n + i0);
 #pragma unroll
-      for (int k = 0; k < W; ++k)
-        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z), "=r"(w[k].w)
-                     : "l"(p + k)
-                     : "memory");
-      memcpy(dst, w, sizeof(S) * VE);
-    };
-    S acc2[VE];
-    load_group(0, acc2);
-    uint32_t q = 1;
-    for (; q + 4 <= a.ks; q += 4) {
-      S g[4][VE];
+        for (int k = 0; k < W; ++k)
+          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z), "=r"(w[k].w)
+                       : "l"(p + k)
+                       : "memory");
+        memcpy(dst, w, sizeof(S) * VE);
+      };
+      S acc2[VE];
+      load_group(0, acc2);
+      uint32_t q = 1;
+      for (; q + 4 <= count; q += 4) {
+        S g[4][VE];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load_group(q + u, g[u]);
+        for (int u = 0; u < 4; ++u) load_group(q + u, g[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int e = 0; e < VE; ++e) acc2[e] = a.op(acc2[e], g[u][e]);
+          for (int e = 0; e < VE; ++e) acc2[e] = a.op(acc2[e], g[u][e]);
+      }
+      for (; q < count; ++q) {
+        S g[VE];
+        load_group(q, g);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc2[e] = a.op(acc2[e], g[e]);
+      }
+      if (is_aligned(out + i0, 32) && (sizeof(S) * VE) % 32 == 0) {
+        store_items<S, VE>(out + i0, acc2);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VE; ++e) out[i0 + e] = acc2[e];
+      }
+      return;
     }
-    for (; q < a.ks; ++q) {
-      S g[VE];
-      load_group(q, g);
 #pragma unroll
-      for (int e = 0; e < VE; ++e) acc2[e] = a.op(acc2[e], g[e]);
+    for (int e = 0; e < VE; ++e) {
+      const uint64_t i = i0 + e;
+      if (i < a.n) {
+        S v = ld_strong(base + i);
+        for (uint32_t q = 1; q < count; ++q) v = a.op(v, ld_strong(base + uint64_t(q) * a.n + i));
+        out[i] = v;
+      }
     }
-    if (is_aligned(a.z + i0, 32) && (sizeof(S) * VE) % 32 == 0) {
-      store_items<S, VE>(a.z + i0, acc2);
-    } else {
-#pragma unroll
-      for (int e = 0; e < VE; ++e) a.z[i0 + e] = acc2[e];
-    }
+  };
+
+  if (a.groups == 1) {
+    fold_rows(a.partials, a.ks, a.z);
     return;
   }
-#pragma unroll
-  for (int e = 0; e < VE; ++e) {
-    const uint64_t i = i0 + e;
-    if (i < a.n) {
-      S v = ld_strong(a.partials + i);
-      for (uint32_t q = 1; q < a.ks; ++q) v = a.op(v, ld_strong(a.partials + uint64_t(q) * a.n + i));
-      a.z[i] = v;
-    }
+  fold_rows(a.partials + uint64_t(q0) * a.n, q1 - q0, a.gpartials + uint64_t(grp) * a.n);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t t = atom_add_acq_rel_gpu(tk + a.groups, 1u);
+    s_last = (t == a.groups - 1);
+    if (s_last) st_relaxed_gpu(tk + a.groups, 0u);
   }
+  __syncthreads();
+  if (!s_last) return;
+  fold_rows(a.gpartials, a.groups, a.z);
 }
 
 // ---------------------------------------------------------------------------
@@ -429,6 +456,7 @@ struct GemvPlan {
   uint64_t cols_per_split;
   uint32_t row_blocks;
   uint64_t grid;
+  uint32_t gsize, groups;  // two-level split fold (gemv_kernel)
 };
 
 template <class T>
@@ -438,7 +466,7 @@ inline GemvPlan plan_gemv(uint64_t n, uint64_t p) {
   static const uint64_t per_sm = [] {
     const char* e = std::getenv("FORGE_GEMV_BLOCKS_PER_SM");  // experiment knob
     const uint64_t v = e ? std::strtoull(e, nullptr, 10) : 3;  // measured best of 1..8 at 16384^2
-    return v < 1 ? 1 : v;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);  // <= 8: primitives.hpp's workspace bound
   }();
   const uint64_t target_blocks = uint64_t(device_props().sm_count) * per_sm;
   uint64_t ks = row_blocks >= target_blocks ? 1 : ceil_div(target_blocks, row_blocks);
@@ -448,10 +476,20 @@ inline GemvPlan plan_gemv(uint64_t n, uint64_t p) {
   uint64_t cps = ceil_div(p, ks);
   ks = ceil_div(p, cps);
   if (ks < 1) ks = 1;
-  return GemvPlan{uint32_t(ks), cps, uint32_t(row_blocks), row_blocks * ks};
+  uint32_t gsize = uint32_t(ks);
+  if (ks > 8) {
+    gsize = 1;
+    while (uint64_t(gsize) * gsize < ks) ++gsize;  // ceil(sqrt(ks))
+  }
+  const uint32_t groups = uint32_t(ceil_div(ks, gsize));
+  return GemvPlan{uint32_t(ks), cps, uint32_t(row_blocks), row_blocks * ks, gsize, groups};
 }
 
-constexpr int kGevmCols = 4;  // columns per warp of gevm_cols_kernel
+// gevm_cols_kernel shape, measured at 16384² f32 (GB/s): 4 columns per warp
+// 6,702 at 79 registers (3 CTAs/SM), 6,877 at <= 64 registers (4 CTAs/SM, no
+// spills), 2 columns per warp 6,533; one column per warp (gevm_kernel) 6,300.
+constexpr int kGevmCols = 4;
+constexpr int kGevmColsMinBlocks = 4;
 
 inline bool gevm_cols_enabled() {
   static const bool v = [] {
@@ -488,11 +526,13 @@ inline uint64_t gevm_ws_bytes(uint64_t n, uint64_t p) {
   return 256 + round_up(p * sizeof(uint32_t), 256) + p * ks * sizeof(S);
 }
 
+// Workspace: [256 | tickets row_blocks x (groups + 1) | partials ks x n | group partials groups x n]
 template <class T, class S>
 inline uint64_t gemv_ws_bytes(uint64_t n, uint64_t p) {
   GemvPlan pl = plan_gemv<T>(n, p);
   if (pl.ks == 1) return 256;
-  return 256 + round_up(uint64_t(pl.row_blocks) * sizeof(uint32_t), 256) + uint64_t(pl.ks) * n * sizeof(S);
+  return 256 + round_up(uint64_t(pl.row_blocks) * (pl.groups + 1) * sizeof(uint32_t), 256) +
+         round_up(uint64_t(pl.ks) * n * sizeof(S), 256) + (pl.groups > 1 ? uint64_t(pl.groups) * n * sizeof(S) : 0);
 }
 
 template <class T, class S, class F2, class Op, bool UsesX, bool Ordered>
@@ -511,7 +551,8 @@ cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, co
   }
   if constexpr (!Ordered) {
     if (cols) {
-      gevm_cols_kernel<T, S, F2, Op, UsesX, kGevmCols><<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
+      gevm_cols_kernel<T, S, F2, Op, UsesX, kGevmCols, kGevmColsMinBlocks>
+          <<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
       return cudaGetLastError();
     }
   }
@@ -525,12 +566,16 @@ cudaError_t launch_gemv(const T* A, uint64_t n, uint64_t p, const T* x, S* z, co
   if (p == 0 || n == 0) return cudaSuccess;
   constexpr int VE = gemv_vec_elems<T>();
   GemvPlan pl = plan_gemv<T>(n, p);
-  GemvArgs<T, S, F2, Op> a{A, x, z, n, p, f, op, pl.ks, pl.cols_per_split, pl.row_blocks, false, nullptr, nullptr};
+  GemvArgs<T, S, F2, Op> a{A,     x,     z,     n,     p,       f,       op, pl.ks, pl.cols_per_split, pl.row_blocks,
+                           false, nullptr, nullptr, pl.gsize, pl.groups, nullptr};
   a.vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && is_aligned(z, 32);
   if (pl.ks > 1) {
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);
-    a.partials = reinterpret_cast<S*>(w + round_up(uint64_t(pl.row_blocks) * sizeof(uint32_t), 256));
+    w += round_up(uint64_t(pl.row_blocks) * (pl.groups + 1) * sizeof(uint32_t), 256);
+    a.partials = reinterpret_cast<S*>(w);
+    w += round_up(uint64_t(pl.ks) * n * sizeof(S), 256);
+    if (pl.groups > 1) a.gpartials = reinterpret_cast<S*>(w);
   }
   gemv_kernel<T, S, F2, Op, UsesX><<<uint32_t(pl.grid), kMatThreads, 0, stream>>>(a);
   return cudaGetLastError();

@@ -314,15 +314,9 @@ struct MapReduceWs {
   }
 };
 
-inline uint32_t mapreduce_blocks_per_sm() {
-  static const uint32_t v = [] {
-    const char* e = std::getenv("FORGE_MR_BLOCKS_PER_SM");  // experiment knob
-    const uint32_t k = e ? uint32_t(std::strtoul(e, nullptr, 10)) : 4u;
-    return k < 1 ? 1u : (k > 256 ? 256u : k);
-  }();
-  return v;
-}
-inline uint32_t mapreduce_max_grid() { return uint32_t(device_props().sm_count) * mapreduce_blocks_per_sm(); }
+// 4 CTAs per SM: measured best of 4..128 (more CTAs lengthen the last CTA's
+// partial fold).  primitives.hpp's workspace bound assumes it.
+inline uint32_t mapreduce_max_grid() { return uint32_t(device_props().sm_count) * 4; }
 
 template <class T>
 inline uint32_t mapreduce_grid(uint64_t n) {

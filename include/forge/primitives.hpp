@@ -223,12 +223,21 @@ inline uint64_t b200_mapreduce_ws_bytes(uint32_t accum_size) {
 // Matrix partials: generous bound covering both kernels' plans for (reduce_len, outputs).
 inline uint64_t b200_mat_ws_bytes(uint32_t accum_size, uint64_t reduce_len, uint64_t outputs) {
   const uint64_t sms = b200_sm_count();
-  // gevm: ks <= max(1, ceil(sms*48 / outputs)), p tickets, outputs*ks partials
-  const uint64_t ks_v = std::max<uint64_t>(1, (sms * 48 + outputs - 1) / std::max<uint64_t>(outputs, 1));
+  // gevm: one-column plan ks <= ceil(sms*48 / outputs); column-group plan (4
+  // columns per warp, ~14 CTAs of 8 warps per SM) ks <= ceil(sms*448 / outputs);
+  // p tickets, outputs*ks partials
+  const uint64_t outs1 = std::max<uint64_t>(outputs, 1);
+  const uint64_t ks_v = std::max<uint64_t>(1, std::max((sms * 48 + outs1 - 1) / outs1, (sms * 448 + outs1 - 1) / outs1));
   const uint64_t gevm = 256 + rup(outputs * 4, 256) + outputs * ks_v * accum_size;
-  // gemv: ks <= sms*4 splits, row_blocks tickets, ks*outputs partials
-  const uint64_t ks_m = std::min<uint64_t>(sms * 4, std::max<uint64_t>(1, (reduce_len + 15) / 16));
-  const uint64_t gemv = 256 + rup(outputs * 4 + 4096, 256) + ks_m * outputs * accum_size;
+  // gemv: ks <= sms*8 splits (3/SM default, FORGE_GEMV_BLOCKS_PER_SM <= 8), row
+  // blocks of >= 256 rows, each with (groups + 1) tickets, groups <= ceil(sqrt(ks)),
+  // ks*outputs split partials + groups*outputs group partials
+  const uint64_t ks_m = std::min<uint64_t>(sms * 8, std::max<uint64_t>(1, (reduce_len + 15) / 16));
+  uint64_t groups = 1;
+  while (groups * groups < ks_m) ++groups;
+  const uint64_t row_blocks = (outputs + 255) / 256;
+  const uint64_t gemv = 256 + rup(row_blocks * (groups + 1) * 4, 256) + rup(ks_m * outputs * accum_size, 256) +
+                        groups * outputs * accum_size;
   return rup(std::max(gevm, gemv), 256);
 }
 
