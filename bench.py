@@ -410,7 +410,24 @@ def breakdown(args, peaks) -> dict:
     dev.fill_synthetic(capi.F32_SUM, src, n1, 1)
     dst = dev.empty(capi.F32_SUM, n1, "S")
     rec("scan_f32_sum_2^20_C1", n1 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, True, src, dst, n1, ws), 20),
-        note="8 MiB, L2-resident: launch/latency bound")
+        note="8 MiB, L2-resident: one call per event pair, host launch latency included")
+    # the same scan as a launch-bound loop captured in a CUDA graph (20 scans per replay)
+    try:
+        gstream = torch.cuda.Stream()
+        gstream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(gstream):
+            for _ in range(3):
+                dev.scan(capi.F32_SUM, True, src, dst, n1, ws)
+        torch.cuda.current_stream().wait_stream(gstream)
+        graph = torch.cuda.CUDAGraph()
+        reps = 20
+        with torch.cuda.graph(graph):
+            for _ in range(reps):
+                dev.scan(capi.F32_SUM, True, src, dst, n1, ws)
+        ms = _time_dev(lambda: graph.replay(), 10) / reps
+        rec("scan_f32_sum_2^20_C1_graph", n1 * 8, ms, note="20 scans per CUDA-graph replay; per-scan time")
+    except Exception as e:  # noqa: BLE001 (report, do not fail the bench)
+        out["scan_f32_sum_2^20_C1_graph"] = {"error": str(e)[:200]}
     # C4 matrices
     nn = 16384
     for name, op, fn in (("gevm_f32_16384^2 (ref matvec)", capi.MV_F32_PLUS_TIMES, dev.matvec),

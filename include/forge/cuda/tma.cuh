@@ -31,16 +31,36 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // rows x 128-byte matrix at `base` (16-byte aligned), boxes of box_rows rows.
+// Encoded maps are cached per thread (8 entries, round robin): a driver
+// encode per call is host latency a small scan would otherwise pay each time.
 inline bool make_rows128_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t box_rows) {
+  struct Entry {
+    const void* base;
+    uint64_t rows;
+    uint32_t box;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[8] = {};
+  static thread_local unsigned next = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* key = static_cast<const char*>(base) + (uint64_t(dev) << 56);  // device-qualified
+  for (const Entry& e : cache)
+    if (e.base == key && e.rows == rows && e.box == box_rows && rows != 0) {
+      *map = e.map;
+      return true;
+    }
   auto enc = tensor_map_encoder();
   if (!enc || rows == 0 || !is_aligned(base, 16)) return false;
   const cuuint64_t dims[2] = {128, rows};
   const cuuint64_t strides[1] = {128};
   const cuuint32_t box[2] = {128, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const bool ok = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (ok) cache[next++ % 8] = Entry{key, rows, box_rows, *map};
+  return ok;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y,

@@ -70,3 +70,31 @@ if what == "copy":
     out["forge_copy"] = round(2 * nb / t(lambda: dev.copy(a, b, nb)) / 1e6, 1)
     out["torch_copy"] = round(2 * nb / t(lambda: b.copy_(a)) / 1e6, 1)
     print(json.dumps({"copy": out}))
+if what == "c1":
+    for n in (1 << 16, 1 << 18, 1 << 20, 1 << 22):
+        op = capi.F32_SUM
+        src = dev.empty(op, n); dev.fill_synthetic(op, src, n, 1); dst = dev.empty(op, n, "S")
+        ms = t(lambda: dev.scan(op, True, src, dst, n, ws), 50)
+        out[f"scan_f32_2^{n.bit_length()-1}_us"] = round(ms * 1e3, 2)
+        if check:
+            from oracle import oracle as orc
+            got = dst.cpu().numpy().view(orc.s_dtype(op))
+            out[f"bad_2^{n.bit_length()-1}"] = orc.check_scan_synthetic(op, True, n, 1, got, 1e-5)[0]
+    print(json.dumps({"c1": out}))
+if what == "c1g":
+    n1 = 1 << 20
+    op = capi.F32_SUM
+    src = dev.empty(op, n1); dev.fill_synthetic(op, src, n1, 1); dst = dev.empty(op, n1, "S")
+    g = torch.cuda.CUDAGraph()
+    for _ in range(3): dev.scan(op, True, src, dst, n1, ws)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        for _ in range(20): dev.scan(op, True, src, dst, n1, ws)
+    out["graph_us_per_scan"] = round(t(lambda: g.replay(), 10) * 1e3 / 20, 2)
+    out["single_us"] = round(t(lambda: dev.scan(op, True, src, dst, n1, ws), 50) * 1e3, 2)
+    if check:
+        from oracle import oracle as orc
+        g.replay(); torch.cuda.synchronize()
+        got = dst.cpu().numpy().view(orc.s_dtype(op))
+        out["bad"] = orc.check_scan_synthetic(op, True, n1, 1, got, 1e-5)[0]
+    print(json.dumps({"c1g": out}))
