@@ -256,6 +256,35 @@ def test_matvec_vecmat(m, op, shape):
         F.release(m, ws)
 
 
+# Shapes that reach the planner's other branches: the 4-column gevm kernel
+# with row splits and a partial last column group (p % 4 != 0), and the gemv
+# two-level split fold (many column splits per row block).
+PLAN_SHAPES = [(65536, 7), (4096, 1021), (2048, 16384), (8, 4099), (24576, 5)]
+
+
+@pytest.mark.parametrize("op", [F.MV_F32_PLUS_TIMES, F.MV_F32_MIN_PLUS])
+@pytest.mark.parametrize("shape", PLAN_SHAPES)
+def test_matvec_vecmat_plans(m, op, shape):
+    n, p = shape
+    A = orc.fill(op, n * p, seed_for(op, n, p, 3))
+    for which in ("matvec", "vecmat"):
+        red, outs = (n, p) if which == "matvec" else (p, n)
+        x = orc.fill(op, red, seed_for(op, n, p, 9))
+        ab, xb = upload(m, op, A), upload(m, op, x)
+        yb = F.create_buffer(m, op, outs, which="S")
+        ws = F.make_mat_workspace(m, op, red, outs)
+        fn = F.matvec if which == "matvec" else F.vecmat
+        for _ in range(2):  # twice: tickets must reset themselves
+            rep = fn(m, F.make_semiring(op), F.make_view(m, ab), n, p, F.make_view(m, xb), F.make_view(m, yb), ws)
+            assert rep.ok
+            got = m.read(yb, outs, F.s_dtype(op))
+            want, ex, sc = (orc.matvec if which == "matvec" else orc.vecmat)(op, A, n, p, x)
+            assert_match(op, got, want, ex, sc, f"{which} {shape}")
+        for b in (ab, xb, yb):
+            m.destroy_buffer(b)
+        F.release(m, ws)
+
+
 def test_matrix_kats(m):
     # identity matvec / vecmat; tropical 2x2.
     op = F.MV_F32_PLUS_TIMES
