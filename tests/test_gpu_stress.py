@@ -1,0 +1,75 @@
+"""Look-back / ticket race stress and compute-sanitizer.
+
+Exact operators make every relaunch comparable bit for bit: a scan whose
+decoupled look-back read a stale or torn tile state, or a reduction whose
+last-CTA fold ran early, shows up as a mismatch against the first launch
+(which itself is checked against the oracle)."""
+from __future__ import annotations
+
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+capi = pytest.importorskip("paper_2603_18695_b200.capi")
+dev = pytest.importorskip("paper_2603_18695_b200.dev")
+F = pytest.importorskip("paper_2603_18695_b200.forge")
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("op", [capi.I32_SUM, capi.MAT2_U32, capi.ARGMAX_F32I32])
+def test_scan_relaunch_stress_tile_boundaries(op):
+    # tile-boundary sizes (T-1, T, T+1, k*T +- 1 for the 8192-item f32 tile and
+    # the 2x4096-item 16-byte tile), 400 launches each, one shared workspace
+    rng = np.random.default_rng(op)
+    tile = 8192
+    sizes = [tile - 1, tile, tile + 1, 7 * tile - 1, 7 * tile + 1, 64 * tile + 1,
+             int(rng.integers(100_000, 2_000_000))]
+    ws = dev.Workspace()
+    for n in sizes:
+        x = dev.empty(op, n)
+        dev.fill_synthetic(op, x, n, 0x57E55 + n)
+        first = dev.empty(op, n, "S")
+        y = dev.empty(op, n, "S")
+        dev.scan(op, True, x, first, n, ws)
+        got = first.cpu().numpy().view(np.uint8).view(F.s_dtype(op))
+        bad, _ = orc.check_scan_synthetic(op, True, n, 0x57E55 + n, got, 1e-5)
+        assert bad == 0
+        for i in range(400):
+            dev.scan(op, True, x, y, n, ws)
+            if i % 50 == 49:
+                assert torch.equal(y, first), f"relaunch {i} of n={n} differs"
+        torch.cuda.synchronize()
+        assert torch.equal(y, first)
+
+
+def test_mapreduce_relaunch_stress():
+    op, n = capi.I32_MAX, 3_000_017
+    x = dev.empty(op, n)
+    dev.fill_synthetic(op, x, n, 91)
+    ws = dev.Workspace()
+    outs = torch.zeros((500, 16), dtype=torch.uint8, device="cuda")
+    for i in range(500):
+        dev.mapreduce(op, x, n, outs[i], ws)
+    torch.cuda.synchronize()
+    want, _, _ = orc.mapreduce_synthetic(op, n, 91)
+    got = outs[:, :4].cpu().numpy().copy().view(np.int32)[:, 0]
+    assert np.all(got == want)
+
+
+@pytest.mark.skipif(shutil.which("compute-sanitizer") is None, reason="compute-sanitizer not on PATH")
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer_clean(tool):
+    r = subprocess.run(["compute-sanitizer", "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        str(ROOT / "tools" / "sanitize_run.py")], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and "sanitize_run ok" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
