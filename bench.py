@@ -447,6 +447,23 @@ def breakdown(args, peaks) -> dict:
     dev.fill_synthetic(capi.UF8_F32_SUM, src, N_C2, 7)
     outb = torch.zeros(16, dtype=torch.uint8, device="cuda")
     rec("mapreduce_uf8_f32_2^30", N_C2, _time_dev(lambda: dev.mapreduce(capi.UF8_F32_SUM, src, N_C2, outb, ws)))
+    del src
+    torch.cuda.empty_cache()
+    # C5 at G = 1: n = 2^33 f32 (32 GiB in + 32 GiB out), exclusive scan and mapreduce;
+    # the sharded path adds an order-preserving shard reduce (tests/test_gpu_fullsize.py)
+    try:
+        n5 = 1 << 33
+        src = dev.empty(capi.F32_SUM, n5)
+        dev.fill_synthetic(capi.F32_SUM, src, n5, 0x5EED0C05)
+        dst = dev.empty(capi.F32_SUM, n5, "S")
+        rec("scan_f32_sum_excl_2^33_C5_G1", n5 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, False, src, dst, n5, ws), 3))
+        del dst
+        o5 = torch.zeros(16, dtype=torch.uint8, device="cuda")
+        rec("mapreduce_f32_sum_2^33_C5_G1", n5 * 4, _time_dev(lambda: dev.mapreduce(capi.F32_SUM, src, n5, o5, ws), 3))
+        del src
+    except Exception as e:  # noqa: BLE001 (e.g. a smaller GPU: report, do not fail the bench)
+        out["C5_G1"] = {"error": str(e)[:200]}
+    torch.cuda.empty_cache()
     return out
 
 

@@ -98,3 +98,27 @@ if what == "c1g":
         got = dst.cpu().numpy().view(orc.s_dtype(op))
         out["bad"] = orc.check_scan_synthetic(op, True, n1, 1, got, 1e-5)[0]
     print(json.dumps({"c1g": out}))
+if what == "bigthen":
+    def mx(tag):
+        nn = 16384
+        op = capi.MV_F32_PLUS_TIMES
+        A = dev.empty(op, nn * nn); dev.fill_synthetic(op, A, nn * nn, 5)
+        x = dev.empty(op, nn); dev.fill_synthetic(op, x, nn, 6)
+        y = dev.empty(op, nn, "S")
+        byts = nn * nn * 4 + 2 * nn * 4
+        out[tag + "_gevm"] = round(byts / t(lambda: dev.matvec(op, A, nn, nn, x, y, ws)) / 1e6, 1)
+        out[tag + "_gemv"] = round(byts / t(lambda: dev.vecmat(op, A, nn, nn, x, y, ws)) / 1e6, 1)
+    mx("before")
+    n5 = 1 << 33
+    src = dev.empty(capi.F32_SUM, n5); dev.fill_synthetic(capi.F32_SUM, src, n5, 1)
+    dst = dev.empty(capi.F32_SUM, n5, "S")
+    dev.scan(capi.F32_SUM, False, src, dst, n5, ws); torch.cuda.synchronize()
+    mx("during")
+    del src, dst
+    mx("after_del")
+    torch.cuda.empty_cache()
+    mx("after_empty")
+    ws2 = dev.Workspace()
+    ws = ws2
+    mx("fresh_ws")
+    print(json.dumps({"bigthen": out}))
