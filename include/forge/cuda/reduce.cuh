@@ -383,36 +383,74 @@ __global__ void __launch_bounds__(kReduceThreads)
   using A = typename M::A;
   constexpr int IT = tile_items<T, S>();
   constexpr uint64_t kTile = uint64_t(kReduceThreads) * IT;
-  __shared__ Opt<A> smem[kReduceThreads / kWarp];
+  constexpr int NW = kReduceThreads / kWarp;
+  constexpr int VE = mr_vec_elems<T>();          // one 32-byte vector per lane per step
+  constexpr uint64_t kStep = uint64_t(kWarp) * VE;
+  constexpr int U = sizeof(T) >= 8 ? 2 : 4;      // steps in flight per warp
+  static_assert(kTile % kStep == 0, "block runs start on whole warp steps");
+  __shared__ Opt<C> wsum[NW];
   __shared__ bool s_last;
   auto cop = [&](const C& x, const C& y) { return CT::op(a.op, x, y); };
   auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
+  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
 
+  // The block's contiguous run splits into NW contiguous warp runs.  A warp
+  // folds its run IN ORDER one coalesced step (32 lanes x 32 bytes) at a
+  // time, U steps in flight: each lane folds its VE elements in order, an
+  // ordered warp reduction combines the lanes, lane 0 folds the step into the
+  // warp's carry (type C).  Warp carries are folded in warp order at the end:
+  // one __syncthreads per block (the tile-by-tile block reduction this
+  // replaces synchronised twice per 4096 elements: 4.7 TB/s).
   const uint64_t ntiles = ceil_div(a.n, kTile);
   const uint64_t t0 = uint64_t(blockIdx.x) * a.tiles_per_block;
   const uint64_t t1 = t0 + a.tiles_per_block < ntiles ? t0 + a.tiles_per_block : ntiles;
-  const bool vec_ok = a.stride == 1 && is_aligned(a.src, items_align<T, IT>());
-  Opt<C> bacc{C{}, false};  // meaningful in thread 0
-  for (uint64_t t = t0; t < t1; ++t) {
-    const uint64_t base = t * kTile + uint64_t(threadIdx.x) * IT;
-    Opt<A> mine{A{}, false};
-    if (base + IT <= a.n && vec_ok) {
-      T x[IT];
-      load_items<T, IT>(a.src + base, x);
-      A v = M::lift(a.f(x[0]));
+  const uint64_t b0 = t0 * kTile, b1 = t1 * kTile < a.n ? t1 * kTile : a.n;
+  const uint64_t nsteps = b1 > b0 ? (b1 - b0) / kStep : 0;
+  const uint64_t s0 = nsteps * warp / NW, s1 = nsteps * (warp + 1) / NW;
+  const bool vec_ok = VE > 1 && a.stride == 1 && is_aligned(a.src, 32);
+  Opt<C> wacc{C{}, false};  // meaningful in lane 0
+  auto fold_step = [&](const Opt<A>& lane_v) {
+    const Opt<A> r = warp_reduce_ordered(aop, lane_v);
+    if (lane == 0 && r.has) {
+      const C rc = M::to_c(r.v);
+      wacc = wacc.has ? Opt<C>{cop(wacc.v, rc), true} : Opt<C>{rc, true};
+    }
+  };
+  if (vec_ok) {
+    for (uint64_t st = s0; st < s1; st += U) {
+      T x[U][VE];
 #pragma unroll
-      for (int k = 1; k < IT; ++k) v = aop(v, M::lift(a.f(x[k])));
-      mine = Opt<A>{v, true};
-    } else {
-      for (int k = 0; k < IT; ++k) {
-        if (base + k < a.n) mine = opt_combine(aop, mine, Opt<A>{M::lift(a.f(a.src[(base + k) * a.stride])), true});
+      for (int u = 0; u < U; ++u)
+        if (st + u < s1) load_items<T, VE>(a.src + b0 + (st + u) * kStep + uint64_t(lane) * VE, x[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (st + u < s1) {
+          A v = M::lift(a.f(x[u][0]));
+#pragma unroll
+          for (int k = 1; k < VE; ++k) v = aop(v, M::lift(a.f(x[u][k])));
+          fold_step(Opt<A>{v, true});
+        }
       }
     }
-    Opt<A> tile = block_reduce_ordered(aop, mine, smem);
-    if (threadIdx.x == 0 && tile.has) {
-      C tc = M::to_c(tile.v);
-      bacc = bacc.has ? Opt<C>{cop(bacc.v, tc), true} : Opt<C>{tc, true};
+  } else {
+    for (uint64_t i0 = b0 + s0 * kStep; i0 < b0 + s1 * kStep; i0 += kWarp) {
+      const uint64_t i = i0 + lane;
+      fold_step(Opt<A>{i < b1 ? M::lift(a.f(a.src[i * a.stride])) : A{}, i < b1});
     }
+  }
+  if (warp == NW - 1) {  // the run's tail (< one step) belongs to the last warp
+    for (uint64_t i0 = b0 + nsteps * kStep; i0 < b1; i0 += kWarp) {
+      const uint64_t i = i0 + lane;
+      fold_step(Opt<A>{i < b1 ? M::lift(a.f(a.src[i * a.stride])) : A{}, i < b1});
+    }
+  }
+  if (lane == 0) wsum[warp] = wacc;
+  __syncthreads();
+  Opt<C> bacc{C{}, false};  // meaningful in thread 0
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+      if (wsum[w].has) bacc = bacc.has ? Opt<C>{cop(bacc.v, wsum[w].v), true} : wsum[w];
   }
   if (threadIdx.x == 0) {
     a.partials[blockIdx.x] = bacc.v;

@@ -122,3 +122,11 @@ if what == "bigthen":
     ws = ws2
     mx("fresh_ws")
     print(json.dumps({"bigthen": out}))
+if what == "ordered":
+    for name, op in (("f32_sum", capi.F32_SUM), ("mat2", capi.MAT2_U32), ("affine", capi.AFFINE_F32)):
+        n = (1 << 30) if op_info(op)["t_size"] <= 4 else (1 << 28)
+        src = dev.empty(op, n); dev.fill_synthetic(op, src, n, 7)
+        o = torch.zeros(32, dtype=torch.uint8, device="cuda")
+        out[name] = round(n * op_info(op)["t_size"] / t(lambda: dev.reduce_ordered(op, src, n, o, ws)) / 1e6, 1)
+        del src
+    print(json.dumps({"ordered": out}))
