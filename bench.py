@@ -298,8 +298,10 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
         "clocks": sampler.summary(),
     }
 
-    if rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e_machine_path(args, n, ops, bufs)
+    if not args.no_e2e:
+        e2e = e2e_machine_path(args, n, ops, bufs, dist, world)
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_breakdown:
         line["breakdown"] = breakdown(args, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -311,12 +313,18 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
         dist.destroy_process_group()
 
 
-def e2e_machine_path(args, n, ops, dev_bufs) -> dict:
-    """The reference-facing call with HOST buffers: Machine.write_bytes from
-    pinned memory (H2D) + forge_mapreduce (kernel + D2H of the S result)."""
+def e2e_machine_path(args, n, ops, dev_bufs, dist=None, world=1) -> dict:
+    """The reference-facing call with HOST buffers on every rank: Machine.write_bytes
+    from pinned memory (H2D) + forge_mapreduce (kernel + D2H of the S result); at
+    N > 1 each rank's host result goes back to its GPU, the partials are
+    all-gathered and folded in rank order, and the final value is read back.
+    Whole-job bytes / the slowest rank's wall time (barriers on both sides)."""
+    import numpy as np
     import torch
 
+    from paper_2603_18695_b200 import dev
     from paper_2603_18695_b200 import forge as F
+    from paper_2603_18695_b200.sharded import _all_gather_bytes
 
     m = F.Machine(torch.cuda.current_device())
     host = {}
@@ -327,23 +335,38 @@ def e2e_machine_path(args, n, ops, dev_bufs) -> dict:
     bufs = {op: F.create_buffer(m, op, n) for op in ops}
     wss = {op: F.make_mapreduce_workspace(m, op) for op in ops}
     views = {op: F.View(bufs[op], 0, n, 1) for op in ops}
+    final = torch.zeros(16, dtype=torch.uint8, device="cuda")
 
     def step():
         for op in ops:
             m.write_ptr(bufs[op], host[op].data_ptr(), host[op].numel())
-            F.mapreduce(m, F.make_semiring(op), views[op], wss[op])
+            val, _ = F.mapreduce(m, F.make_semiring(op), views[op], wss[op])
+            if world > 1:
+                part = torch.from_numpy(np.array([val]).view(np.uint8).copy()).cuda()
+                gath = _all_gather_bytes(part, world)
+                dev.fold(op, gath, world, final)
+                final.cpu()  # the job's result on the host
 
     for _ in range(max(1, min(args.warmup, 2))):
         step()
     k = max(2, min(args.steps, 5))
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(k):
         step()
     dt = time.perf_counter() - t0
+    if dist:
+        dist.barrier()
+        tt = torch.tensor([dt], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
     byts = sum(host[op].numel() for op in ops)
-    res = {"value": byts * k / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": byts,
-           "d2h_bytes_per_step": sum(F.op_info(op)["s_size"] for op in ops),
-           "path": "forge_write_bytes(pinned host) + forge_mapreduce (host result)", "steps": k}
+    res = {"value": world * byts * k / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": world * byts,
+           "d2h_bytes_per_step": world * sum(F.op_info(op)["s_size"] for op in ops),
+           "path": "forge_write_bytes(pinned host) + forge_mapreduce (host result)"
+                   + (" + all-gather of partials, rank-order fold, D2H of the result" if world > 1 else ""),
+           "steps": k}
     for op in ops:
         F.release(m, wss[op])
         m.destroy_buffer(bufs[op])
