@@ -267,6 +267,42 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
     bytes_step = sum(n * F.op_info(op)["t_size"] for op in ops)
     value = world * bytes_step * args.steps / (ms * 1e-3) / 1e9
 
+    elems_per_s = world * n * len(ops) * args.steps / (ms * 1e-3)
+
+    # C5-style sharded exclusive scan on the same ranks (reduce-then-scan: ordered
+    # shard reduce, all-gather of shard totals, rank-order fold, carry-seeded
+    # local scan), 2^28 f32 per GPU, device-timed, max over ranks
+    sharded_scan = None
+    if not args.no_sharded_scan:
+        from paper_2603_18695_b200 import sharded
+        ns = 1 << 28
+        xs = dev.empty(capi.F32_SUM, ns)
+        dev.fill_synthetic(capi.F32_SUM, xs, ns, 0x5EED0C05, index_base=rank * ns)
+        ys = dev.empty(capi.F32_SUM, ns, "S")
+        be = sharded.DeviceBackend()
+        for _ in range(3):
+            sharded.sharded_scan(capi.F32_SUM, False, xs, ys, ns, backend=be)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record(stream)
+        for _ in range(reps):
+            sharded.sharded_scan(capi.F32_SUM, False, xs, ys, ns, backend=be)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1) / reps
+        if dist:
+            tt = torch.tensor([sms], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            sms = float(tt.item())
+        sharded_scan = {"workload": "exclusive scan f32 sum, 2^28 per GPU (C5 shape, weak scaling)",
+                        "gbs": world * ns * 8 / (sms * 1e-3) / 1e9, "elems_per_s": world * ns / (sms * 1e-3),
+                        "ms": sms, "hbm_bytes_per_gpu": 3 * ns * 4,
+                        "note": "GB/s counts the algorithmic 8 B per element; the reduce-then-scan reads the input twice"}
+        del xs, ys
+
     # roofline: the mapreduce kernel alone, events on its stream
     kern_ev.clear()
     for _ in range(3):
@@ -293,11 +329,14 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
                    "n_per_gpu": n, "global_n": n * world, "bytes_per_gpu_per_step": bytes_step,
                    "l2": "inputs 4 GiB each >> 126 MB L2; no flush needed",
                    "parallelism": f"shard{world}"},
+        "elems_per_s": elems_per_s,
         "roofline": roofline,
         "gpu_launches": args.steps * len(ops) * (2 if world > 1 else 1),
         "clocks": sampler.summary(),
     }
 
+    if sharded_scan is not None:
+        line["sharded_scan"] = sharded_scan
     if not args.no_e2e:
         e2e = e2e_machine_path(args, n, ops, bufs, dist, world)
         if rank == 0:
@@ -399,9 +438,11 @@ def breakdown(args, peaks) -> dict:
     out = {}
     peak = peaks["hbm_gbs"]
 
-    def rec(name, byts, ms, **kw):
+    def rec(name, byts, ms, elems=None, **kw):
         gbs = byts / (ms * 1e-3) / 1e9
         out[name] = {"gbs": round(gbs, 1), "ms": round(ms, 4), "frac": round(gbs / peak, 4), **kw}
+        if elems:
+            out[name]["elems_per_s"] = float(f"{elems / (ms * 1e-3):.4g}")
 
     ws = dev.Workspace()
     # vcopy calibration: 2 GiB copy
@@ -425,14 +466,14 @@ def breakdown(args, peaks) -> dict:
         ms = _time_dev(lambda: dev.scan(op, incl, src, dst, n, ws))
         from paper_2603_18695_b200.forge import op_info
         inf = op_info(op)
-        rec(name, n * (inf["t_size"] + inf["s_size"]), ms)
+        rec(name, n * (inf["t_size"] + inf["s_size"]), ms, elems=n)
         del src, dst
     # C1: 2^20 scan (L2-resident, launch-bound)
     n1 = 1 << 20
     src = dev.empty(capi.F32_SUM, n1)
     dev.fill_synthetic(capi.F32_SUM, src, n1, 1)
     dst = dev.empty(capi.F32_SUM, n1, "S")
-    rec("scan_f32_sum_2^20_C1", n1 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, True, src, dst, n1, ws), 20),
+    rec("scan_f32_sum_2^20_C1", n1 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, True, src, dst, n1, ws), 20), elems=n1,
         note="8 MiB, L2-resident: one call per event pair, host launch latency included")
     # the same scan as a launch-bound loop captured in a CUDA graph (20 scans per replay)
     try:
@@ -448,7 +489,7 @@ def breakdown(args, peaks) -> dict:
             for _ in range(reps):
                 dev.scan(capi.F32_SUM, True, src, dst, n1, ws)
         ms = _time_dev(lambda: graph.replay(), 10) / reps
-        rec("scan_f32_sum_2^20_C1_graph", n1 * 8, ms, note="20 scans per CUDA-graph replay; per-scan time")
+        rec("scan_f32_sum_2^20_C1_graph", n1 * 8, ms, elems=n1, note="20 scans per CUDA-graph replay; per-scan time")
     except Exception as e:  # noqa: BLE001 (report, do not fail the bench)
         out["scan_f32_sum_2^20_C1_graph"] = {"error": str(e)[:200]}
     # C4 matrices
@@ -463,13 +504,14 @@ def breakdown(args, peaks) -> dict:
         dev.fill_synthetic(op, x, nn, 6)
         y = dev.empty(op, nn, "S")
         ms = _time_dev(lambda: fn(op, A, nn, nn, x, y, ws))
-        rec(name, nn * nn * 4 + 2 * nn * 4, ms)
+        rec(name, nn * nn * 4 + 2 * nn * 4, ms, elems=nn * nn)
         del A, x, y
     # C2 extra: uf8 promotion
     src = dev.empty(capi.UF8_F32_SUM, N_C2)
     dev.fill_synthetic(capi.UF8_F32_SUM, src, N_C2, 7)
     outb = torch.zeros(16, dtype=torch.uint8, device="cuda")
-    rec("mapreduce_uf8_f32_2^30", N_C2, _time_dev(lambda: dev.mapreduce(capi.UF8_F32_SUM, src, N_C2, outb, ws)))
+    rec("mapreduce_uf8_f32_2^30", N_C2, _time_dev(lambda: dev.mapreduce(capi.UF8_F32_SUM, src, N_C2, outb, ws)),
+        elems=N_C2)
     del src
     torch.cuda.empty_cache()
     # C5 at G = 1: n = 2^33 f32 (32 GiB in + 32 GiB out), exclusive scan and mapreduce;
@@ -479,10 +521,12 @@ def breakdown(args, peaks) -> dict:
         src = dev.empty(capi.F32_SUM, n5)
         dev.fill_synthetic(capi.F32_SUM, src, n5, 0x5EED0C05)
         dst = dev.empty(capi.F32_SUM, n5, "S")
-        rec("scan_f32_sum_excl_2^33_C5_G1", n5 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, False, src, dst, n5, ws), 3))
+        rec("scan_f32_sum_excl_2^33_C5_G1", n5 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, False, src, dst, n5, ws), 3),
+            elems=n5)
         del dst
         o5 = torch.zeros(16, dtype=torch.uint8, device="cuda")
-        rec("mapreduce_f32_sum_2^33_C5_G1", n5 * 4, _time_dev(lambda: dev.mapreduce(capi.F32_SUM, src, n5, o5, ws), 3))
+        rec("mapreduce_f32_sum_2^33_C5_G1", n5 * 4, _time_dev(lambda: dev.mapreduce(capi.F32_SUM, src, n5, o5, ws), 3),
+            elems=n5)
         del src
     except Exception as e:  # noqa: BLE001 (e.g. a smaller GPU: report, do not fail the bench)
         out["C5_G1"] = {"error": str(e)[:200]}
@@ -500,6 +544,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-breakdown", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded-scan", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -120,10 +120,14 @@ def sharded_scan(op: int, inclusive: bool, local_src, local_dst, n_local: int, b
                  group=None) -> torch.Tensor:
     """Scan of the global array whose rank-ordered shards are `local_src`;
     writes this rank's slice of the global scan into `local_dst`.  Returns the
-    gathered shard totals (bytes, rank order)."""
+    gathered shard totals (bytes, rank order), or None for a single rank (plain
+    local scan)."""
     be = backend or DeviceBackend()
     rank, world = _world(group)
     ss = be.s_size(op)
+    if world == 1:  # one shard: no carry to compute, no exchange
+        be.scan(op, inclusive, local_src, local_dst, n_local, None)
+        return None
     total = be.new_bytes(ss)
     be.reduce_ordered(op, local_src, n_local, total)
     totals = _all_gather_bytes(total, world, group)
