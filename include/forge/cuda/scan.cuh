@@ -444,10 +444,18 @@ constexpr uint32_t kSmemScanDyn = kSmemTileBytes + 1024;                 // + sw
 //
 // Resident CTAs per SM the kernel is compiled for: 6 x 33 KB (R = 1) or
 // 3 x 65 KB (R = 2) of tile (Little's law) — <= 40 / 80
-// registers; wide carries get 2/3 of that.
+// registers.
+// Wide carries (f64 affine / quaternion, 16-byte structs) get the same 6
+// CTAs/SM: measured affine 2^28 at 4 / 5 / 6 CTAs/SM (64 / 48 / 40 registers,
+// the last with 20 bytes of spills): 3,744 / 4,193 / 4,252 GB/s.
+#ifndef FORGE_SCAN_WIDE_BLOCKS
+#define FORGE_SCAN_WIDE_BLOCKS 6
+#endif
+constexpr int scan_env_wide_blocks() { return FORGE_SCAN_WIDE_BLOCKS; }
+
 template <class S, class Op, int R>
 constexpr int scan_smem_min_blocks() {
-  return (sizeof(typename ScanMath<S, Op>::C) <= 8 ? 6 : 4) / R;
+  return (sizeof(typename ScanMath<S, Op>::C) <= 8 ? 6 : scan_env_wide_blocks()) / R;
 }
 
 constexpr uint32_t scan_smem_dyn(int R) { return uint32_t(R) * kSmemTileBytes + 1024; }
