@@ -1,5 +1,6 @@
 """Per-tile event timing of the carry-chain scan kernel (development tool).
-python tools/trace_chain.py [op] [log2n]   (sets FORGE_SCAN_PATH=chain, FORGE_SCAN_TRACE=1)"""
+python tools/trace_chain.py [op] [log2n]   (sets FORGE_SCAN_PATH=chain, FORGE_SCAN_TRACE=1;
+needs a `make EXPERIMENTS=1` build)"""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["FORGE_SCAN_TRACE"] = "1"
