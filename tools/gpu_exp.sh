@@ -1,5 +1,3 @@
-# Scratch GPU experiment (development; overwritten per experiment): run with
-#   gpurun -- bash tools/gpu_exp.sh
-mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x -k "scan" --timeout 900 -p no:randomly > gpurun_out/pytest_scan.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/pytest_scan.log
-timeout 300 python tools/probe.py scan > gpurun_out/exp_wide.log 2>&1
+# Scratch GPU experiment (development; overwritten per experiment)
+mkdir -p gpurun_out; : > gpurun_out/exp.log
+for b in 2 3 4 5 3 4; do FORGE_GEMV_BLOCKS_PER_SM=$b timeout 120 python tools/probe.py matrix | tail -1 | sed "s/^/bps=$b /" >> gpurun_out/exp.log 2>&1; done
