@@ -1,3 +1,5 @@
 # Scratch GPU experiment (development; overwritten per experiment)
 mkdir -p gpurun_out; : > gpurun_out/exp.log
-for b in 2 3 4 5 3 4; do FORGE_GEMV_BLOCKS_PER_SM=$b timeout 120 python tools/probe.py matrix | tail -1 | sed "s/^/bps=$b /" >> gpurun_out/exp.log 2>&1; done
+FORGE_SCAN_LOOKBACK=3 timeout 300 python tools/probe.py scan --check | sed "s/^/groups /" >> gpurun_out/exp.log 2>&1
+timeout 300 python tools/probe.py scan | sed "s/^/flat /" >> gpurun_out/exp.log 2>&1
+FORGE_SCAN_LOOKBACK=3 timeout 300 python tools/trace_scan.py 0 28 2>&1 | grep -v "^  \|^ }" | sed "s/^/groups trace /" >> gpurun_out/exp.log 2>&1
