@@ -85,12 +85,11 @@ class ClockSampler:
                 nv.nvmlDeviceGetCurrentClocksThrottleReasons
             self._nvml = nv
 
+            self._h, self._get_reasons = h, get_reasons
+
             def loop():
                 while not self._stop.is_set():
-                    try:
-                        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), int(get_reasons(h))))
-                    except Exception:
-                        pass
+                    self.sample_now()
                     time.sleep(0.002)
 
             self._t = threading.Thread(target=loop, daemon=True)
@@ -98,6 +97,16 @@ class ClockSampler:
         except Exception:
             self._nvml = None
         return self
+
+    def sample_now(self):
+        """One synchronous sample (also called from the timed loop while the GPU is busy)."""
+        if self._nvml is None:
+            return
+        try:
+            nv = self._nvml
+            self.samples.append((nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM), int(self._get_reasons(self._h))))
+        except Exception:
+            pass
 
     def __exit__(self, *exc):
         self._stop.set()
@@ -256,6 +265,9 @@ def forge_arm(args, rank: int, world: int, local_rank: int) -> None:
         for _ in range(args.steps):
             step()
         t1.record(stream)
+        # every step is queued: sample while the GPU works through them (an NVML
+        # query takes milliseconds — never between enqueues, it would starve the GPU)
+        sampler.sample_now()
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
