@@ -8,6 +8,7 @@ tensors of n * sizeof bytes).  All calls are asynchronous and stream-ordered.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 
 import torch
 
@@ -35,10 +36,17 @@ def _ptr(t) -> C.c_void_p:
     return C.c_void_p(t.data_ptr())
 
 
-def workspace_bytes(prim: int, op: int, n: int, p_cols: int = 0) -> int:
+@functools.lru_cache(maxsize=256)
+def _workspace_bytes(device: int, prim: int, op: int, n: int, p_cols: int) -> int:
     out = C.c_uint64()
     check(_lib().forge_dev_workspace_bytes(prim, op, n, p_cols, C.byref(out)))
     return out.value
+
+
+def workspace_bytes(prim: int, op: int, n: int, p_cols: int = 0) -> int:
+    """Bytes of device workspace a call needs (cached per device and shape: a
+    ctypes round trip per launch is host latency small launches would pay)."""
+    return _workspace_bytes(torch.cuda.current_device(), prim, op, n, p_cols)
 
 
 class Workspace:
