@@ -1,3 +1,3 @@
 # Scratch GPU experiment (development; overwritten per experiment)
 mkdir -p gpurun_out
-timeout 600 python bench.py > gpurun_out/bench_final.log 2>&1; echo "bench_rc=$?" >> gpurun_out/bench_final.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_step.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-breakdown --no-sharded-scan > gpurun_out/bench_ncu.log 2>&1
