@@ -42,6 +42,10 @@
 #include "forge/cuda/scan.cuh"
 #endif
 
+#ifdef __CUDACC__
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (ranges around primitive calls)
+#endif
+
 namespace forge::prim {
 
 using intr::View;
@@ -297,9 +301,19 @@ Workspace make_mat_workspace(Machine& m, uint64_t reduce_len, uint64_t outputs,
 
 namespace detail {
 
+// NVTX range around every primitive call (header-only NVTX v3: a no-op unless
+// a profiler such as nsys injects itself).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 template <class Fn>
 LaunchReport run_timed(Machine& m, const RunOptions& opt, const char* name, uint64_t elems,
                        Fn&& launch) {
+  NvtxRange range(name);
   LaunchReport rep;
   rep.buffers.resize(m.buffer_count());
   uint64_t launches = 0;

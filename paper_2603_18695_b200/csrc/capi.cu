@@ -622,6 +622,7 @@ int forge_dev_workspace_bytes(forge_primitive prim, forge_op op, uint64_t n, uin
 
 int forge_dev_mapreduce(forge_op op, const void* src, uint64_t n, void* out_dev, void* ws,
                         uint64_t ws_bytes, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_mapreduce");
   return guarded([&]() -> int {
     int rc = menu::visit1(op, [&](auto e) -> int {
       using E = decltype(e);
@@ -648,6 +649,7 @@ int forge_dev_mapreduce(forge_op op, const void* src, uint64_t n, void* out_dev,
 
 int forge_dev_reduce_ordered(forge_op op, const void* src, uint64_t n, void* out_dev, void* ws,
                              uint64_t ws_bytes, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_reduce_ordered");
   return guarded([&]() -> int {
     int rc = menu::visit1(op, [&](auto e) -> int {
       using E = decltype(e);
@@ -672,6 +674,7 @@ int forge_dev_reduce_ordered(forge_op op, const void* src, uint64_t n, void* out
 int forge_dev_scan(forge_op op, int32_t inclusive, const void* src, void* dst, uint64_t n,
                    const void* carry_in_dev, void* total_out_dev, void* ws, uint64_t ws_bytes,
                    void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_scan");
   return guarded([&]() -> int {
     int rc = menu::visit1(op, [&](auto e) -> int {
       using E = decltype(e);
@@ -693,6 +696,7 @@ int forge_dev_scan(forge_op op, int32_t inclusive, const void* src, void* dst, u
 
 int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* y,
                      void* ws, uint64_t ws_bytes, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_matvec");
   return guarded([&]() -> int {
     int rc = menu::visit2(op, [&](auto e) -> int {
       using E = decltype(e);
@@ -717,6 +721,7 @@ int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, co
 
 int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* z,
                      void* ws, uint64_t ws_bytes, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_vecmat");
   return guarded([&]() -> int {
     int rc = menu::visit2(op, [&](auto e) -> int {
       using E = decltype(e);
@@ -735,6 +740,7 @@ int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, co
 
 int forge_dev_fold(forge_op op, const void* values_dev, uint32_t count, int32_t exclusive_upto,
                    void* out_dev, int32_t* has_out_dev, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_fold");
   return guarded([&]() -> int {
     auto go = [&](auto e) -> int {
       using E = decltype(e);
@@ -751,6 +757,7 @@ int forge_dev_fold(forge_op op, const void* values_dev, uint32_t count, int32_t 
 }
 
 int forge_dev_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_copy");
   return guarded([&]() -> int {
     auto st = static_cast<cudaStream_t>(stream);
     if (bytes % 4 == 0 && cuda::is_aligned(src, 4) && cuda::is_aligned(dst, 4))
@@ -765,6 +772,7 @@ int forge_dev_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
 
 int forge_dev_fill_synthetic(forge_op op, void* dst, uint64_t n, uint64_t seed, uint64_t index_base,
                              int32_t variant, void* stream) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_dev_fill_synthetic");
   return guarded([&]() -> int {
     if (n == 0) return FORGE_OK;
     uint64_t grid = (n + 255) / 256;
