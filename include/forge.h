@@ -277,14 +277,27 @@ int forge_mapreduce_2d(forge_machine* m, forge_semiring spec, forge_view A, uint
 int forge_vcopy(forge_machine* m, forge_view src, forge_view dst, uint32_t nitem,
                 const forge_arch_params* params, forge_launch_report* report);
 
+/* MutationFlags (primitives.hpp:64-67), the reference's ordering ablation, for
+ * the calling thread's subsequent forge_scan / forge_dev_scan calls.  TEST ONLY:
+ * relax_scan_flag = 1 makes the scan accept tile states left by EARLIER launches
+ * on the same workspace (the epoch tag is ignored), a deliberately broken
+ * publication protocol that the relaunch stress tests must detect
+ * (tests/test_gpu_stress.py).  relax_mapreduce_flag is accepted and ignored: the
+ * B200 mapreduce never waits on another block's flag.  (0, 0) restores the
+ * product protocol. */
+int forge_set_mutation_flags(int32_t relax_scan_flag, int32_t relax_mapreduce_flag);
+
 /* vload_pattern (intrinsics.hpp:190, intrinsics.cpp:29-33). segs has room for 16. */
 int forge_vload_pattern(uint64_t offset, uint32_t nitem, uint32_t* segs, uint32_t* count);
 
 /* ---------------------------------------------------------------------------
  * Device-pointer layer: stream-ordered, asynchronous, no host synchronisation.
  * `stream` is a cudaStream_t (NULL = the legacy default stream).  `ws` is caller
- * device memory of at least forge_dev_workspace_bytes(...) bytes, zeroed once
- * before first use (cudaMemset); the kernels leave it re-usable.  A workspace
+ * device memory of at least forge_dev_workspace_bytes(...) bytes (full speed;
+ * a scan also accepts less, down to packed tile states), zeroed once before
+ * first use (cudaMemset); the kernels leave it re-usable.  One workspace may
+ * serve several primitives and shapes in turn: the library re-zeroes the part
+ * a layout needs when the workspace last served another layout.  A workspace
  * must not be shared by launches in flight at the same time. */
 int forge_dev_workspace_bytes(forge_primitive prim, forge_op op, uint64_t n, uint64_t p_cols,
                               uint64_t* bytes);

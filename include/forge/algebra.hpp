@@ -121,14 +121,48 @@ FORGE_HD AffineT<F> affine_compose(const AffineT<F>& p, const AffineT<F>& q) {
   return AffineT<F>{q.a * p.a, q.a * p.b + q.b};
 }
 
+// ---- order-independent f32 max / min.  The reference's
+// `a >= b ? a : b` is neither commutative on ±0 nor associative with NaN, so
+// a GPU tree and a sequential fold could disagree bit-wise on such inputs.
+// Here: any NaN operand gives the canonical quiet NaN (0x7fc00000); -0 < +0
+// (max(-0, +0) = +0, min(-0, +0) = -0).  On ordinary values it equals the
+// reference operator exactly.
+FORGE_HD float canonical_nan_f32() { return std::numeric_limits<float>::quiet_NaN(); }
+FORGE_HD bool is_nan_f32(float x) { return x != x; }
+FORGE_HD bool sign_bit_f32(float x) {
+#if defined(__CUDA_ARCH__)
+  return __float_as_uint(x) >> 31;
+#else
+  return std::signbit(x);
+#endif
+}
+FORGE_HD float fmax_total(float a, float b) {
+  if (is_nan_f32(a) || is_nan_f32(b)) return canonical_nan_f32();
+  if (a == b) return sign_bit_f32(a) ? b : a;  // equal: differ at most in the sign of zero
+  return a > b ? a : b;
+}
+FORGE_HD float fmin_total(float a, float b) {
+  if (is_nan_f32(a) || is_nan_f32(b)) return canonical_nan_f32();
+  if (a == b) return sign_bit_f32(a) ? a : b;
+  return a < b ? a : b;
+}
+
 struct ArgMax {
   float v;
   int32_t i;
 };
 
+// max by v, ties to the smaller i.  NaN values rank above every number (the
+// arg-max of data containing NaN is its first NaN); -0 == +0 ties by index.
+// A total preorder on v, so the op is associative and commutative for every
+// input, NaN included.
 FORGE_HD ArgMax argmax_combine(const ArgMax& a, const ArgMax& b) {
-  if (a.v > b.v) return a;
-  if (b.v > a.v) return b;
+  const bool an = is_nan_f32(a.v), bn = is_nan_f32(b.v);
+  if (an != bn) return an ? a : b;
+  if (!an) {
+    if (a.v > b.v) return a;
+    if (b.v > a.v) return b;
+  }
   return a.i <= b.i ? a : b;
 }
 

@@ -401,6 +401,18 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
 // ---------------------------------------------------------------------------
 // Host-side launch helpers.
 
+// Development / experiment knobs.  Only builds compiled with -DFORGE_DEV
+// (`make DEV=1` -> libforge_dev.so) read them from the environment; the
+// product library uses the tuned defaults and never calls getenv.
+#ifdef FORGE_DEV
+inline uint32_t dev_knob(const char* name, uint32_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? uint32_t(std::strtoul(e, nullptr, 10)) : dflt;
+}
+#else
+constexpr uint32_t dev_knob(const char*, uint32_t dflt) { return dflt; }
+#endif
+
 struct DeviceProps {
   int sm_count = 148;
   int device = -1;
@@ -418,6 +430,23 @@ inline const DeviceProps& device_props() {
   }
   return cache;
 }
+
+// Workspace layout registry (defined in libforge.so, csrc/machine.cu).  Every
+// primitive's kernels keep their own invariants on the workspace bytes they
+// use (arrival tickets at zero, scan epochs), restored by the kernels
+// themselves at the end of every launch — but two primitives (or two shapes of
+// the matrix kernels) place tickets and partials at different offsets, so a
+// workspace passed to another layout would see the previous layout's partials
+// as tickets.  Each launch therefore claims `ws` for its layout `tag`; when
+// the pointer was last used with another tag (or is unknown), the first
+// `zero_bytes` bytes are zeroed on `stream` before the kernel (the reference
+// zero-fills its flags on every launch, primitives.hpp:374, :464-466, :759).
+cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t stream);
+
+// Layout tags.
+constexpr uint64_t kWsTagTicket = 1;  // mapreduce / ordered reduce: ticket word at offset 0
+constexpr uint64_t kWsTagScan = 2;    // scan: control block + epoch-tagged tile states
+inline uint64_t ws_tag(uint64_t kind, uint64_t a, uint64_t b = 0) { return kind | (a << 8) | (b << 40); }
 
 __host__ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }

@@ -464,8 +464,7 @@ inline GemvPlan plan_gemv(uint64_t n, uint64_t p) {
   constexpr int VE = gemv_vec_elems<T>();
   const uint64_t row_blocks = ceil_div(n, uint64_t(kMatThreads) * VE);
   static const uint64_t per_sm = [] {
-    const char* e = std::getenv("FORGE_GEMV_BLOCKS_PER_SM");  // experiment knob
-    const uint64_t v = e ? std::strtoull(e, nullptr, 10) : 3;  // measured best of 1..8 at 16384^2
+    const uint64_t v = dev_knob("FORGE_GEMV_BLOCKS_PER_SM", 3);  // measured best of 1..8 at 16384^2
     return v < 1 ? 1 : (v > 8 ? 8 : v);  // <= 8: primitives.hpp's workspace bound
   }();
   const uint64_t target_blocks = uint64_t(device_props().sm_count) * per_sm;
@@ -492,10 +491,7 @@ constexpr int kGevmCols = 4;
 constexpr int kGevmColsMinBlocks = 4;
 
 inline bool gevm_cols_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("FORGE_GEVM_COLS");
-    return !(e && e[0] == '0');
-  }();
+  static const bool v = dev_knob("FORGE_GEVM_COLS", 1) != 0;
   return v;
 }
 
@@ -547,7 +543,9 @@ cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, co
   if (pl.ks > 1) {
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);
-    a.partials = reinterpret_cast<S*>(w + round_up(p * sizeof(uint32_t), 256));
+    const uint64_t tbytes = round_up(p * sizeof(uint32_t), 256);
+    a.partials = reinterpret_cast<S*>(w + tbytes);
+    if (const cudaError_t e = ws_claim(ws, ws_tag(3, tbytes), 256 + tbytes, stream); e != cudaSuccess) return e;
   }
   if constexpr (!Ordered) {
     if (cols) {
@@ -572,7 +570,11 @@ cudaError_t launch_gemv(const T* A, uint64_t n, uint64_t p, const T* x, S* z, co
   if (pl.ks > 1) {
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);
-    w += round_up(uint64_t(pl.row_blocks) * (pl.groups + 1) * sizeof(uint32_t), 256);
+    const uint64_t tbytes = round_up(uint64_t(pl.row_blocks) * (pl.groups + 1) * sizeof(uint32_t), 256);
+    if (const cudaError_t e = ws_claim(ws, ws_tag(4, pl.row_blocks, pl.groups), 256 + tbytes, stream);
+        e != cudaSuccess)
+      return e;
+    w += tbytes;
     a.partials = reinterpret_cast<S*>(w);
     w += round_up(uint64_t(pl.ks) * n * sizeof(S), 256);
     if (pl.groups > 1) a.gpartials = reinterpret_cast<S*>(w);

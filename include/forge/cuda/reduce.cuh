@@ -356,6 +356,7 @@ cudaError_t launch_mapreduce(const T* src, uint64_t n, uint64_t stride, const F&
   const uint32_t grid = mapreduce_grid<T>(stride == 1 ? n : n * 4);
   MapReduceArgs<T, S, F, Op> a{src, n, stride, f, op, nullptr, nullptr, nullptr, out_dev, out_has_dev};
   MapReduceWs<S>::carve(ws, mapreduce_max_grid(), a.ticket, a.partials, a.part_has);
+  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream); e != cudaSuccess) return e;
   mapreduce_kernel<T, S, F, Op, mr_unroll<T>()><<<grid, kReduceThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }
@@ -536,6 +537,7 @@ cudaError_t launch_reduce_ordered(const T* src, uint64_t n, uint64_t stride, con
   grid = ntiles ? ceil_div(ntiles, per) : 1;
   OrderedReduceArgs<T, S, F, Op, C> a{src, n, stride, f, op, per, nullptr, nullptr, nullptr, out_dev, out_has_dev};
   OrderedReduceWs<S, Op>::carve(ws, cap, a.ticket, a.partials, a.part_has);
+  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream); e != cudaSuccess) return e;
   reduce_ordered_kernel<T, S, F, Op><<<uint32_t(grid), kReduceThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }

@@ -50,16 +50,22 @@ namespace forge::cuda {
 
 constexpr int kScanThreads = 256;
 constexpr uint32_t kPartial = 1, kPrefix = 2;
-constexpr int kLookbackPerThread = 4;     // max polls per thread of the block-wide look-back (pipe kernel)
 constexpr int kLookbackRows = 1;          // warp look-back: rows of 32 predecessors per round trip
 constexpr uint32_t kStateSlotWords = 32;  // 256-byte tile-state slots
 constexpr int kRowBytes = 128;            // smem kernel: bytes of T per thread row
-constexpr uint32_t kLookbackSkipProbe = 99;  // FORGE_SCAN_LOOKBACK value of the no-look-back probe
+constexpr uint32_t kLookbackSkipProbe = 99;  // FORGE_DEV builds only: FORGE_SCAN_LOOKBACK=99 skips the look-back
+                                             // (WRONG results; the look-back-free ceiling probe of DESIGN.md §7)
+
+constexpr int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
 
 template <class C>
 struct TileStateIO {
   static constexpr int SW = Words<C>::N;  // 32-bit chunks of the carry
-  static constexpr int STRIDE = SW <= 1 ? 1 : SW <= 2 ? 2 : SW <= 4 ? 4 : SW <= 8 ? 8 : 16;
+  static constexpr int STRIDE = next_pow2(SW);  // 64-bit words per state: every chunk, any sizeof(C)
 
   static __device__ __forceinline__ void write(uint64_t* states, uint64_t tile, uint32_t stride,
                                                uint32_t epoch, uint32_t kind, const C& v) {
@@ -90,37 +96,14 @@ struct TileStateIO {
       for (int i = 0; i < STRIDE; i += 2) ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
     }
   }
-  static __device__ __forceinline__ uint32_t decode(const uint64_t (&raw)[STRIDE], uint32_t epoch, C& v) {
+  static __device__ __forceinline__ uint32_t decode(const uint64_t (&raw)[STRIDE], uint32_t epoch, C& v,
+                                                   uint32_t epoch_mask = 0x3fffffffu) {
     const uint32_t hi = uint32_t(raw[0] >> 32);
     bool same = true;
 #pragma unroll
     for (int i = 1; i < SW; ++i) same &= uint32_t(raw[i] >> 32) == hi;
     const uint32_t kind = hi & 3u;
-    if (!same || kind == 0 || (hi >> 2) != (epoch & 0x3fffffffu)) return 0;
-    Words<C> w;
-#pragma unroll
-    for (int i = 0; i < SW; ++i) w.w[i] = uint32_t(raw[i]);
-    v = from_words<C>(w);
-    return kind;
-  }
-
-  // Returns the kind (0 = not yet valid for this epoch) and the value.
-  static __device__ __forceinline__ uint32_t read(const uint64_t* states, uint64_t tile, uint32_t stride,
-                                                  uint32_t epoch, C& v) {
-    const uint64_t* p = states + tile * stride;
-    uint64_t raw[STRIDE];
-    if constexpr (STRIDE == 1) {
-      raw[0] = ld_relaxed_gpu(p);
-    } else {
-#pragma unroll
-      for (int i = 0; i < STRIDE; i += 2) ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
-    }
-    const uint32_t hi = uint32_t(raw[0] >> 32);
-    bool same = true;
-#pragma unroll
-    for (int i = 1; i < SW; ++i) same &= uint32_t(raw[i] >> 32) == hi;
-    const uint32_t kind = hi & 3u;
-    if (!same || kind == 0 || (hi >> 2) != (epoch & 0x3fffffffu)) return 0;
+    if (!same || kind == 0 || ((hi >> 2) & epoch_mask) != (epoch & epoch_mask)) return 0;
     Words<C> w;
 #pragma unroll
     for (int i = 0; i < SW; ++i) w.w[i] = uint32_t(raw[i]);
@@ -144,9 +127,11 @@ struct ScanArgs {
   uint32_t* ctrl;     // [0] ticket, [2] epoch
   uint32_t ntiles;
   uint32_t state_stride;  // 64-bit words per tile state slot
-  uint32_t lookback;      // 0: warp 0 polls 32 predecessors; k: 256*k predecessors block-wide
-  uint64_t* trace;        // optional per-tile phase timestamps (FORGE_SCAN_TRACE), else null
-  uint32_t backoff_ns;    // look-back: sleep between polls of INVALID states (FORGE_SCAN_BACKOFF_NS)
+  uint32_t lookback;      // 0 (FORGE_DEV builds: kLookbackSkipProbe skips the look-back)
+  uint64_t* trace;        // FORGE_DEV builds: per-tile phase timestamps (own buffer), else null
+  uint32_t backoff_ns;    // look-back: sleep between polls of INVALID states (0; FORGE_DEV knob)
+  uint32_t epoch_mask;    // 0x3fffffff; 0 = the relax_scan_flag ablation (MutationFlags,
+                          // primitives.hpp:64-67): stale states of earlier launches are accepted
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -186,7 +171,7 @@ using ScanSharedOf = ScanShared<typename ScanMath<S, Op>::A, typename ScanMath<S
 template <int Q, class IO, class C, class COp>
 __device__ __forceinline__ Opt<C> warp_lookback(const uint64_t* states, uint32_t stride, uint32_t epoch,
                                                 int64_t tile, const COp& cop, uint64_t* trace, uint64_t trace_tile,
-                                                uint32_t backoff_ns = 0) {
+                                                uint32_t backoff_ns, uint32_t epoch_mask) {
   constexpr uint32_t kEmpty = 4;  // position before tile 0
   const unsigned lane = lane_id();
   Opt<C> carry{C{}, false};
@@ -210,7 +195,7 @@ __device__ __forceinline__ Opt<C> warp_lookback(const uint64_t* states, uint32_t
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         if (kind[q] == 0) {
-          kind[q] = IO::decode(raw[q], epoch, val[q]);
+          kind[q] = IO::decode(raw[q], epoch, val[q], epoch_mask);
           all &= kind[q] != 0;
         }
       }
@@ -318,7 +303,7 @@ __device__ __forceinline__ void block_exclusive_prefix(
       // development ceiling probe (FORGE_SCAN_LOOKBACK=99): no look-back, WRONG results
     } else if (warp == 0) {
       carry = warp_lookback<kLookbackRows, IO, C>(a.states, a.state_stride, epoch, int64_t(tile), cop, a.trace, tile,
-                                                  a.backoff_ns);
+                                                  a.backoff_ns, a.epoch_mask);
     }
     if (threadIdx.x == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
@@ -638,569 +623,65 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
   }
 }
 
-// ---------------------------------------------------------------------------
-// Fast path v3: persistent, software-pipelined tiles.
-//
-// Measured on the one-tile-per-CTA kernel (profiles/): a tile lives ~8 us, of
-// which ~5.4 us is the look-back, spent waiting for the most recent
-// predecessors' PARTIALs — whose publication is gated by their own TMA
-// landing-time tail (head-of-line blocking).  Here a producer warp claims
-// tickets and keeps kPipeStages tiles in flight with 2-D TMA; the 256 consumer
-// threads run, per iteration,
-//     A(next tile): fold rows from smem, block scan, publish PARTIAL
-//     look-back(current tile) -> PREFIX        (its predecessors' PARTIALs were
-//                                                published an iteration earlier)
-//     C(current tile): running prefixes written back into the smem tile,
-//                      one TMA tensor store, stage released to the producer.
-// Deadlock-freedom without co-residency: tiles are claimed in ticket order and
-// each CTA processes its claims in order, so the owner of the smallest
-// unfinished tile is always at that tile's A or look-back, which waits only on
-// smaller (finished) tiles.
-
-constexpr int kPipeStages = 3;
-constexpr int kPipeThreads = kScanThreads + kWarp;  // + 1 producer warp
-constexpr uint32_t kPipeDyn = kPipeStages * kSmemTileBytes + 1024;
-constexpr uint32_t kNoTile = 0xffffffffu;
-
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kScanThreads) : "memory");
-}
-
-template <class A, class C>
-struct PipeShared {
-  Opt<A> warp[kScanThreads / kWarp];
-  Opt<A> carry;
-  int first[kScanThreads / kWarp];
-  Opt<C> lb[kScanThreads / kWarp];
-};
-
-template <class S, class Op>
-using PipeSharedOf = PipeShared<typename ScanMath<S, Op>::A, typename ScanMath<S, Op>::C>;
-
-// Block scan of the 256 row totals: returns the row's exclusive prefix WITHIN
-// the tile; `agg` receives the tile aggregate (all threads).
-template <class A, class Sh, class AOp>
-__device__ __forceinline__ Opt<A> pipe_tile_scan(const AOp& aop, const Opt<A>& tot, Sh& sh, Opt<A>& agg) {
-  constexpr int NW = kScanThreads / kWarp;
-  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
-  const Opt<A> incl = warp_scan_incl(aop, tot);
-  if (lane == kWarp - 1) sh.warp[warp] = incl;
-  consumer_sync();
-  if (warp == 0) {
-    Opt<A> w = lane < NW ? sh.warp[lane] : Opt<A>{A{}, false};
-    w = warp_scan_incl(aop, w);
-    if (lane < NW) sh.warp[lane] = w;
-  }
-  consumer_sync();
-  agg = sh.warp[NW - 1];
-  const Opt<A> warp_ex = warp > 0 ? sh.warp[warp - 1] : Opt<A>{A{}, false};
-  Opt<A> lane_ex = shfl_up_opt(incl, 1);
-  if (lane == 0) lane_ex.has = false;
-  const Opt<A> ex = opt_combine(aop, warp_ex, lane_ex);
-  consumer_sync();  // sh.warp is reused by the next tile
-  return ex;
-}
-
-// Block-wide look-back for tile > 0 whose aggregate is already PARTIAL.
-// Publishes PREFIX; returns the tile's exclusive carry to every consumer thread.
-template <class T, class S, class F, class Op>
-__device__ __forceinline__ Opt<typename ScanMath<S, Op>::A> pipe_lookback(
-    const ScanArgs<T, S, F, Op>& a, uint64_t tile, uint32_t epoch, const typename ScanMath<S, Op>::C& agg_c,
-    PipeSharedOf<S, Op>& sh) {
-  using M = ScanMath<S, Op>;
-  using A = typename M::A;
-  using C = typename M::C;
-  using IO = TileStateIO<C>;
-  constexpr int NW = kScanThreads / kWarp;
-  constexpr int LB = kLookbackPerThread;
-  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
-  auto cop = [&](const C& x, const C& y) { return M::CT::op(a.op, x, y); };
-  const int lbn = int(a.lookback == 0 ? 1u : (a.lookback < uint32_t(LB) ? a.lookback : uint32_t(LB)));
-  const int WIN = kScanThreads * lbn;
-  Opt<C> carry{C{}, false};  // meaningful in thread 0
-  int64_t hi = int64_t(tile);
-  for (;;) {
-    C val[LB];
-    uint32_t kind[LB];
-    int first = WIN;
-#pragma unroll
-    for (int q = 0; q < LB; ++q) {
-      kind[q] = 0;
-      val[q] = C{};
-      const int64_t j = hi - 1 - int64_t(threadIdx.x) * lbn - q;
-      if (q < lbn && j >= 0) {
-        while ((kind[q] = IO::read(a.states, uint64_t(j), a.state_stride, epoch, val[q])) == 0) {
-        }
-      }
-      if (kind[q] == kPrefix && first == WIN) first = int(threadIdx.x) * lbn + q;
-    }
-    const unsigned pm = __ballot_sync(kFullMask, first < WIN);
-    const int wfirst = __shfl_sync(kFullMask, first, pm ? __ffs(int(pm)) - 1 : 0);
-    if (lane == 0) sh.first[warp] = pm ? wfirst : WIN;
-    consumer_sync();
-    int pl = WIN;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) pl = sh.first[w] < pl ? sh.first[w] : pl;
-    const bool found = pl < WIN;
-    // Fold positions 0..pl (position 0 = tile hi-1), older always on the LEFT.
-    Opt<C> v{C{}, false};
-#pragma unroll
-    for (int q = LB - 1; q >= 0; --q) {
-      const int pos = int(threadIdx.x) * lbn + q;
-      if (kind[q] != 0 && pos <= pl) v = opt_combine(cop, v, Opt<C>{val[q], true});
-    }
-#pragma unroll
-    for (unsigned d = 1; d < kWarp; d <<= 1) {
-      Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
-      if (lane + d < kWarp) v = opt_combine(cop, got, v);
-    }
-    if (lane == 0) sh.lb[warp] = v;
-    consumer_sync();
-    if (threadIdx.x == 0) {
-      Opt<C> window{C{}, false};
-#pragma unroll
-      for (int w = NW - 1; w >= 0; --w) window = opt_combine(cop, window, sh.lb[w]);
-      carry = opt_combine(cop, window, carry);
-    }
-    consumer_sync();  // sh.first / sh.lb reuse
-    if (found) break;
-    hi -= WIN;
-  }
-  if (threadIdx.x == 0) {
-    const C inclusive_c = cop(carry.v, agg_c);
-    IO::write(a.states, tile, a.state_stride, epoch, kPrefix, inclusive_c);
-    sh.carry = Opt<A>{M::from_c(carry.v), true};
-    if (tile == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(inclusive_c);
-  }
-  consumer_sync();
-  const Opt<A> r = sh.carry;
-  consumer_sync();
-  return r;
-}
-
-template <class T, class S, class F, class Op, bool Inclusive>
-__global__ void __launch_bounds__(kPipeThreads)
-    scan_pipe_kernel(const ScanArgs<T, S, F, Op> a, const __grid_constant__ CUtensorMap tmap,
-                     const __grid_constant__ CUtensorMap tmap_out, bool tma_store) {
-  using M = ScanMath<S, Op>;
-  using A = typename M::A;
-  using C = typename M::C;
-  using IO = TileStateIO<C>;
-  constexpr int IT = smem_scan_items<T>();
-  constexpr int EPC = 16 / int(sizeof(T));
-  constexpr int NCH = kRowBytes / 16;
-  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
-  extern __shared__ unsigned char dyn_smem[];
-  __shared__ __align__(8) uint64_t full[kPipeStages];
-  __shared__ __align__(8) uint64_t empty[kPipeStages];
-  __shared__ uint32_t ring[kPipeStages];
-  __shared__ uint32_t s_epoch;
-  __shared__ PipeSharedOf<S, Op> sh;
-  auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
-  unsigned char* stage_mem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
-  const bool tail_partial = (a.n % kTile) != 0;
-
-  if (threadIdx.x == kScanThreads) {
-    for (int s = 0; s < kPipeStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (threadIdx.x >= kScanThreads) {
-    // ---- producer: epoch first, then tickets (acq_rel) in order, each CTA
-    // until its first failure -> exactly ntiles + gridDim.x claims per launch.
-    if (threadIdx.x != kScanThreads) return;
-    const uint32_t epoch = ld_acquire_gpu(a.ctrl + 2);
-    s_epoch = epoch;
-    for (uint32_t it = 0;; ++it) {
-      const int s = int(it % kPipeStages);
-      if (it >= uint32_t(kPipeStages)) mbar_wait(&empty[s], ((it / kPipeStages) - 1) & 1u);
-      uint32_t t = atom_add_acq_rel_gpu(a.ctrl + 0, 1u);
-      if (t == a.ntiles + gridDim.x - 1) {
-        st_relaxed_gpu(a.ctrl + 0, 0u);
-        st_relaxed_gpu(a.ctrl + 2, epoch + 1u);
-      }
-      if (t >= a.ntiles) t = kNoTile;
-      ring[s] = t;
-      if (t != kNoTile && !(tail_partial && t == a.ntiles - 1)) {
-        mbar_arrive_expect_tx(&full[s], kSmemTileBytes);
-        tma_load_2d(stage_mem + size_t(s) * kSmemTileBytes, &tmap, 0, int(t) * kScanThreads, &full[s]);
-      } else {
-        mbar_arrive(&full[s]);  // end marker, or the partial last tile (read from global)
-      }
-      if (t == kNoTile) return;
-    }
-  }
-
-  // ---- consumers
-  // A(tile): fold the rows, block scan, publish; returns the row's in-tile exclusive prefix.
-  auto phase_a = [&](uint32_t tile, int s, uint32_t epoch, C& agg_c) -> Opt<A> {
-    const bool fulltile = !(tail_partial && tile == a.ntiles - 1);
-    const uint64_t base = uint64_t(tile) * kTile + uint64_t(threadIdx.x) * IT;
-    const unsigned char* tm = stage_mem + size_t(s) * kSmemTileBytes;
-    Opt<A> tot{A{}, false};
-    if (fulltile) {
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const uint4 v = lds128(tm + swz128(threadIdx.x, c));
-        T x[EPC];
-        memcpy(x, &v, 16);
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) {
-          const A y = M::lift(a.f(x[e]));
-          tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
-        }
-      }
-      tot.has = true;
-    } else {
-      const uint64_t avail = base < a.n ? a.n - base : 0;
-      const int cnt = avail >= uint64_t(IT) ? IT : int(avail);
-      for (int k = 0; k < cnt; ++k) {
-        const A y = M::lift(a.f(a.src[base + k]));
-        tot.v = k == 0 ? y : aop(tot.v, y);
-      }
-      tot.has = cnt > 0;
-    }
-    Opt<A> agg;
-    const Opt<A> ex = pipe_tile_scan(aop, tot, sh, agg);
-    agg_c = M::to_c(agg.v);
-    if (threadIdx.x == 0) {
-      if (tile == 0) {
-        C pre = agg_c;
-        if (a.carry_in) pre = M::CT::op(a.op, M::to_c(M::lift(*a.carry_in)), pre);
-        IO::write(a.states, 0, a.state_stride, epoch, kPrefix, pre);
-        if (a.ntiles == 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
-      } else {
-        IO::write(a.states, tile, a.state_stride, epoch, kPartial, agg_c);
-      }
-    }
-    return ex;
-  };
-
-  // C(tile): running prefixes from `run` (the row's exclusive prefix).
-  auto phase_c = [&](uint32_t tile, int s, Opt<A> run) {
-    const bool fulltile = !(tail_partial && tile == a.ntiles - 1);
-    const uint64_t base = uint64_t(tile) * kTile + uint64_t(threadIdx.x) * IT;
-    unsigned char* tm = stage_mem + size_t(s) * kSmemTileBytes;
-    if (fulltile) {
-      const bool vec = is_aligned(a.dst + base, 16);
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const uint4 v = lds128(tm + swz128(threadIdx.x, c));
-        T x[EPC];
-        memcpy(x, &v, 16);
-        S o[EPC];
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) {
-          const A y = M::lift(a.f(x[e]));
-          if constexpr (Inclusive) {
-            run.v = run.has ? aop(run.v, y) : y;
-            run.has = true;
-            o[e] = M::lower(run.v);
-          } else {
-            o[e] = run.has ? M::lower(run.v) : a.identity;
-            run.v = run.has ? aop(run.v, y) : y;
-            run.has = true;
-          }
-        }
-        if constexpr (sizeof(S) == sizeof(T)) {
-          if (tma_store) {
-            uint4 w;
-            memcpy(&w, o, 16);
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(tm + swz128(threadIdx.x, c))),
-                         "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
-                         : "memory");
-            continue;
-          }
-        }
-        S* d = a.dst + base + uint64_t(c) * EPC;
-        if (vec) {
-          store_items<S, EPC>(d, o);
-        } else {
-#pragma unroll
-          for (int e = 0; e < EPC; ++e) d[e] = o[e];
-        }
-      }
-      if (sizeof(S) == sizeof(T) && tma_store) {
-        fence_proxy_async_smem();
-        consumer_sync();
-        if (threadIdx.x == 0) {
-          tma_store_2d(&tmap_out, 0, int(tile) * kScanThreads, tm);
-          tma_store_commit();
-          tma_store_wait_read();
-        }
-      } else {
-        consumer_sync();
-      }
-    } else {
-      const uint64_t avail = base < a.n ? a.n - base : 0;
-      const int cnt = avail >= uint64_t(IT) ? IT : int(avail);
-      for (int k = 0; k < cnt; ++k) {
-        const A y = M::lift(a.f(a.src[base + k]));
-        if constexpr (Inclusive) {
-          run.v = run.has ? aop(run.v, y) : y;
-          run.has = true;
-          a.dst[base + k] = M::lower(run.v);
-        } else {
-          a.dst[base + k] = run.has ? M::lower(run.v) : a.identity;
-          run.v = run.has ? aop(run.v, y) : y;
-          run.has = true;
-        }
-      }
-      consumer_sync();
-    }
-    if (threadIdx.x == 0) mbar_arrive(&empty[s]);  // stage free for the producer
-  };
-
-  uint32_t it = 0;
-  int s_cur = 0;
-  mbar_wait(&full[0], 0);
-  uint32_t cur = ring[0];
-  if (cur == kNoTile) return;
-  const uint32_t epoch = s_epoch;
-  C agg_cur;
-  trace_mark(a.trace, cur, 0);
-  Opt<A> ex_cur = phase_a(cur, 0, epoch, agg_cur);
-  trace_mark(a.trace, cur, 1);
-  for (;;) {
-    const uint32_t it_next = it + 1;
-    const int s_next = int(it_next % kPipeStages);
-    mbar_wait(&full[s_next], (it_next / kPipeStages) & 1u);
-    const uint32_t nxt = ring[s_next];
-    C agg_next{};
-    Opt<A> ex_next{A{}, false};
-    if (nxt != kNoTile) {
-      trace_mark(a.trace, nxt, 0);
-      ex_next = phase_a(nxt, s_next, epoch, agg_next);
-      trace_mark(a.trace, nxt, 1);
-    }
-    // look-back of the current tile
-    Opt<A> carry{A{}, false};
-    trace_mark(a.trace, cur, 2);
-    if (cur == 0) {
-      if (a.carry_in) carry = Opt<A>{M::lift(*a.carry_in), true};
-    } else {
-      carry = pipe_lookback(a, cur, epoch, agg_cur, sh);
-    }
-    trace_mark(a.trace, cur, 3);
-    phase_c(cur, s_cur, opt_combine(aop, carry, ex_cur));
-    trace_mark(a.trace, cur, 4);
-    if (nxt == kNoTile) break;
-    cur = nxt;
-    s_cur = s_next;
-    agg_cur = agg_next;
-    ex_cur = ex_next;
-    it = it_next;
-  }
-}
-
-}  // namespace forge::cuda
-
-#include "forge/cuda/scan_ws.cuh"       // warp-specialised kernel (uses the machinery above)
-#include "forge/cuda/scan_cluster.cuh"  // cluster-tiled kernel (uses the machinery above)
-#include "forge/cuda/scan_chain.cuh"    // persistent kernel with a carry chain (uses the machinery above)
-
-namespace forge::cuda {
 
 // ---------------------------------------------------------------------------
 // Workspace + launch.
 
+// Workspace: [256-byte control block (ticket, epoch) | one state slot per tile].
+// Full-speed slots are 256 bytes (kSlotWords); a smaller
+// workspace is accepted down to packed slots (kMinSlotWords) at some look-back
+// speed.  The size depends on S only, so a workspace made for S
+// (make_scan_workspace<S>) fits every T: the bound is the larger of the
+// general kernel's tiles (256 x 64 bytes of S) at packed slots and the smem
+// kernel's tiles of a sizeof(S)-byte T at full slots.
 template <class T, class S, class Op>
 struct ScanWs {
   using C = typename CarryTraits<S, Op>::C;
   static constexpr uint64_t kTileGeneral = uint64_t(kScanThreads) * scan_items<S>();
-  static constexpr uint64_t kTileSmem = uint64_t(kScanThreads) * smem_scan_items<T>();
-  static constexpr uint32_t kSlotWords =
-      TileStateIO<C>::STRIDE > kStateSlotWords ? TileStateIO<C>::STRIDE : kStateSlotWords;
-  static uint64_t tiles(uint64_t n) {
-    const uint64_t g = ceil_div(n, kTileGeneral), s = ceil_div(n, kTileSmem);
-    return g > s ? g : s;
+  static constexpr uint32_t kMinSlotWords = uint32_t(TileStateIO<C>::STRIDE);
+  static constexpr uint32_t kSlotWords = kMinSlotWords > kStateSlotWords ? kMinSlotWords : kStateSlotWords;
+  static constexpr uint64_t kSizedTile =  // smem tile of a T with sizeof(T) == sizeof(S)
+      sizeof(S) >= 16 ? 2 * uint64_t(kScanThreads) * (kRowBytes / 16)
+                      : uint64_t(kScanThreads) * (sizeof(S) <= uint64_t(kRowBytes) ? kRowBytes / sizeof(S) : 1);
+  static uint64_t min_bytes_for(uint64_t tiles) { return 256 + (tiles ? tiles : 1) * kMinSlotWords * 8; }
+  static uint64_t bytes(uint64_t n) {
+    const uint64_t full = 256 + (n ? ceil_div(n, kSizedTile) : 1) * kSlotWords * 8;
+    const uint64_t packed = min_bytes_for(ceil_div(n, kTileGeneral));
+    return full > packed ? full : packed;
   }
-  static uint64_t bytes(uint64_t n) { return 256 + tiles(n) * kSlotWords * sizeof(uint64_t); }
+  // Largest slot stride (64-bit words, power of two, <= kSlotWords) that fits
+  // `tiles` slots in `ws_bytes`; 0 when even packed slots do not fit.
+  static uint32_t slot_words(uint64_t tiles, uint64_t ws_bytes) {
+    for (uint32_t w = kSlotWords; w >= kMinSlotWords && w > 0; w >>= 1)
+      if (256 + (tiles ? tiles : 1) * uint64_t(w) * 8 <= ws_bytes) return w;
+    return 0;
+  }
 };
 
-// Experiment knobs (defaults are the tuned values):
-//   FORGE_SCAN_LOOKBACK    polls per thread of a block-wide look-back (0 = warp 0, window 32)
-//   FORGE_SCAN_STATE_WORDS 64-bit words between consecutive tile states (<= 32)
-//   FORGE_SCAN_PATH        "regs" forces the register-staged kernel
-inline uint32_t scan_env_u32(const char* name, uint32_t dflt) {
-  const char* e = std::getenv(name);
-  return e ? uint32_t(std::strtoul(e, nullptr, 10)) : dflt;
-}
+// Development knobs (FORGE_DEV builds only; constants otherwise).
 inline uint32_t scan_lookback_mode() {
-  static const uint32_t v = scan_env_u32("FORGE_SCAN_LOOKBACK", 0);
+  static const uint32_t v = dev_knob("FORGE_SCAN_LOOKBACK", 0);
   return v;
 }
 inline uint32_t scan_backoff_ns() {
-  static const uint32_t v = scan_env_u32("FORGE_SCAN_BACKOFF_NS", 0);
-  return v;
-}
-inline uint32_t scan_state_words_override() {
-  static const uint32_t v = scan_env_u32("FORGE_SCAN_STATE_WORDS", 0);
+  static const uint32_t v = dev_knob("FORGE_SCAN_BACKOFF_NS", 0);
   return v;
 }
 inline bool scan_force_regs() {
-  static const bool v = [] {
-    const char* e = std::getenv("FORGE_SCAN_PATH");
-    return e && std::strcmp(e, "regs") == 0;
-  }();
+  static const bool v = dev_knob("FORGE_SCAN_REGS", 0) != 0;
   return v;
 }
-
-// Default fast path: one TMA tile per CTA (measured fastest, profiles/);
-// FORGE_SCAN_PATH=pipe selects the persistent pipelined kernel.
-// 0 = one tile per CTA, 1 = pipelined, 2 = warp-specialised.
-inline int scan_path() {
-  static const int v = [] {
-    const char* e = std::getenv("FORGE_SCAN_PATH");
-    if (e && std::strcmp(e, "chain") == 0) return 3;
-    if (e && std::strcmp(e, "ws") == 0) return 2;
-    if (e && std::strcmp(e, "pipe") == 0) return 1;
-    return 0;
-  }();
+inline bool scan_no_tma_store() {
+  static const bool v = dev_knob("FORGE_SCAN_NO_TMA_STORE", 0) != 0;
   return v;
-}
-
-template <class T, class S, class F, class Op, bool Inclusive>
-inline uint32_t scan_ws_grid(uint64_t ntiles) {
-  static thread_local int cached_dev = -1, cached_occ = 1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev) {
-    cudaFuncSetAttribute(scan_ws_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(ws_dyn_bytes<T, S, Op>()));
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_ws_kernel<T, S, F, Op, Inclusive>, kWsThreads,
-                                                  ws_dyn_bytes<T, S, Op>());
-    cached_occ = occ < 1 ? 1 : occ;
-    cached_dev = dev;
-  }
-  const uint64_t cap = uint64_t(device_props().sm_count) * cached_occ;
-  return uint32_t(ntiles < cap ? ntiles : cap);
-}
-
-inline bool scan_use_one_tile_kernel() {
-  static const bool v = [] {
-    const char* e = std::getenv("FORGE_SCAN_PATH");
-    return !(e && std::strcmp(e, "pipe") == 0);
-  }();
-  return v;
-}
-
-// Persistent grid: #SM x resident CTAs of the pipelined kernel.
-template <class T, class S, class F, class Op, bool Inclusive>
-inline uint32_t scan_pipe_grid(uint64_t ntiles) {
-  static thread_local int cached_dev = -1, cached_occ = 1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != cached_dev) {
-    cudaFuncSetAttribute(scan_pipe_kernel<T, S, F, Op, Inclusive>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kPipeDyn));
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_pipe_kernel<T, S, F, Op, Inclusive>, kPipeThreads,
-                                                  kPipeDyn);
-    cached_occ = occ < 1 ? 1 : occ;
-    cached_dev = dev;
-  }
-  const uint64_t cap = uint64_t(device_props().sm_count) * cached_occ;
-  return uint32_t(ntiles < cap ? ntiles : cap);
-}
-
-// CTAs per look-back tile of the cluster kernel (FORGE_SCAN_CLUSTER; 1 = the
-// one-tile-per-CTA kernel).
-inline uint32_t scan_cluster_size() {
-  static const uint32_t v = [] {
-    uint32_t k = scan_env_u32("FORGE_SCAN_CLUSTER", 1);
-    return k == 0 ? 1u : (k > uint32_t(kMaxScanCluster) ? uint32_t(kMaxScanCluster) : k);
-  }();
-  return v;
-}
-
-template <class T, class S, class F, class Op, bool Inclusive>
-cudaError_t launch_scan_cluster(const ScanArgs<T, S, F, Op>& a, const CUtensorMap& tmap,
-                                const CUtensorMap& tmap_out, bool tstore, uint32_t K, uint32_t nsub,
-                                cudaStream_t stream) {
-  static thread_local int done_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  auto kern = scan_cluster_kernel<T, S, F, Op, Inclusive>;
-  if (done_dev != dev) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemScanDyn));
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         int(scan_env_u32("FORGE_SCAN_CARVEOUT", 100)));
-    done_dev = dev;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(uint32_t(ceil_div(nsub, K)) * K);
-  cfg.blockDim = dim3(kScanThreads);
-  cfg.dynamicSmemBytes = kSmemScanDyn;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = K;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, tmap, tmap_out, tstore);
-}
-
-// Persistent carry-chain kernel: cooperative grid of #SM x resident CTAs,
-// FORGE_SCAN_CHAIN_CTAS (1|2) per SM, as many ring stages as fit
-// (FORGE_SCAN_STAGES caps), lag D (FORGE_SCAN_LAG) between reduce and scan.
-template <class T, class S, class F, class Op, bool Inclusive>
-cudaError_t launch_scan_chain(const ScanArgs<T, S, F, Op>& a, const CUtensorMap& tmap, const CUtensorMap& tmap_out,
-                              bool tstore, cudaStream_t stream) {
-  using L = ChainLayout<S, Op>;
-  auto kern = scan_chain_kernel<T, S, F, Op, Inclusive>;
-  static thread_local int cached_dev = -1;
-  static thread_local int ns = 0, lag = 0, occ = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (cached_dev != dev) {
-    const uint32_t per_sm = scan_env_u32("FORGE_SCAN_CHAIN_CTAS", 1) >= 2 ? 2u : 1u;
-    const uint32_t budget = (per_sm == 1 ? 232448u : 114688u) - 2048u;  // dynamic smem per CTA
-    int fit = int((budget - 1024u) / L::kStageBytes);
-    fit = fit > kChainMaxStages ? kChainMaxStages : fit;
-    const int req = int(scan_env_u32("FORGE_SCAN_STAGES", 0));
-    ns = req >= 2 && req < fit ? req : fit;
-    const int half = ns / 2 > 1 ? ns / 2 : 1;
-    const int dflt_lag = ns - 1 - half > 1 ? ns - 1 - half : 1;
-    const int lreq = int(scan_env_u32("FORGE_SCAN_LAG", 0));
-    lag = lreq >= 1 && lreq <= ns - 1 ? lreq : dflt_lag;
-    if (ns < lag + 1) return cudaErrorInvalidConfiguration;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::dyn_bytes(ns)));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kChainThreads, L::dyn_bytes(ns));
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    cached_dev = dev;
-  }
-  const uint64_t cap = uint64_t(device_props().sm_count) * uint64_t(occ);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(uint32_t(a.ntiles < cap - 1 ? a.ntiles : cap - 1) + 1);  // + the chain CTA
-  cfg.blockDim = dim3(kChainThreads);
-  cfg.dynamicSmemBytes = L::dyn_bytes(ns);
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency is what guarantees progress
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, tmap, tmap_out, tstore, ns, lag);
 }
 
 // 32 KB sub-tiles per CTA tile of the default kernel: measured (f32 / i32 /
 // affine / argmax / Mat2 at 2^28, GB/s) R=1: 4896 / 4941 / 3747 / 4612 / 3801,
-// R=2: 4635 / 4658 / 3491 / 4264 / 4532 — so R = 2 only for 16-byte elements.
-// (The R = 2 kernel is instantiated for those only; FORGE_SCAN_SUBTILES=1
-// forces R = 1 for them.)
+// R=2: 4635 / 4658 / 3491 / 4264 / 4532 — so R = 2 for 16-byte elements only.
 template <class T>
-inline int scan_subtiles() {
-  static const int v = int(scan_env_u32("FORGE_SCAN_SUBTILES", 0));
-  return sizeof(T) >= 16 && v != 1 ? 2 : 1;
+constexpr int scan_subtiles() {
+  return sizeof(T) >= 16 ? 2 : 1;
 }
 
 template <class T, class S, class F, class Op, bool Inclusive, int R>
@@ -1214,96 +695,88 @@ cudaError_t launch_scan_smem(const ScanArgs<T, S, F, Op>& a, const CUtensorMap& 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_smem_dyn(R)));
     // Maximum shared-memory carveout: residency (tiles in flight) is what
     // hides the look-back latency; the kernel barely uses L1.
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         int(scan_env_u32("FORGE_SCAN_CARVEOUT", 100)));
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     done_dev = dev;
   }
   kern<<<a.ntiles, kScanThreads, scan_smem_dyn(R), stream>>>(a, tmap, tmap_out, tstore);
   return cudaGetLastError();
 }
 
+#ifdef FORGE_DEV
+// Per-tile phase timestamps (tools/trace_scan.py): a buffer of its own, never
+// the caller's workspace.  8 words per tile; fetched with forge_dev_scan_trace.
+inline uint64_t*& scan_trace_buffer() {
+  static uint64_t* p = nullptr;
+  return p;
+}
+inline uint64_t& scan_trace_words() {
+  static uint64_t w = 0;
+  return w;
+}
+inline uint64_t* scan_trace_for(uint64_t tiles) {
+  if (!dev_knob("FORGE_SCAN_TRACE", 0)) return nullptr;
+  if (scan_trace_words() < tiles * 8) {
+    if (scan_trace_buffer()) cudaFree(scan_trace_buffer());
+    scan_trace_buffer() = nullptr;
+    if (cudaMalloc(&scan_trace_buffer(), tiles * 64) != cudaSuccess) return nullptr;
+    scan_trace_words() = tiles * 8;
+  }
+  return scan_trace_buffer();
+}
+#endif
+
+// Launch.  `ws` holds `ws_bytes` bytes (>= ScanWs::min_bytes_for(tiles) of the
+// kernel that runs; ScanWs::bytes(n) gives full-speed slots), zeroed once at
+// creation.  Returns cudaErrorInvalidValue when the workspace is too small
+// (callers check first and raise WorkspaceTooSmall).
+// `relax_epoch` is the relax_scan_flag ablation (MutationFlags): states of
+// earlier launches on the same workspace are accepted — a deliberately broken
+// protocol that the relaunch stress tests must catch (tests/test_gpu_stress.py).
 template <class T, class S, class F, class Op>
 cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_stride, uint64_t n,
                         bool inclusive, const F& f, const Op& op, const S& identity,
-                        const S* carry_in, S* total_out, void* ws, cudaStream_t stream) {
+                        const S* carry_in, S* total_out, void* ws, uint64_t ws_bytes, cudaStream_t stream,
+                        bool relax_epoch = false) {
   using WsT = ScanWs<T, S, Op>;
   if (n == 0) return cudaSuccess;
-  if (WsT::tiles(n) >= (1ull << 31)) return cudaErrorInvalidValue;
+  if (ceil_div(n, WsT::kTileGeneral) >= (1ull << 31)) return cudaErrorInvalidValue;
   ScanArgs<T, S, F, Op> a{src,      dst,      n,         src_stride, dst_stride,
                           f,        op,       identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
-                          static_cast<uint32_t*>(ws), 0u, WsT::kSlotWords, scan_lookback_mode(), nullptr,
-                          scan_backoff_ns()};
-  if (scan_env_u32("FORGE_SCAN_TRACE", 0))  // development: phase timestamps after the tile states
-    a.trace = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + WsT::bytes(n));
-  {
-    const uint32_t w = scan_state_words_override();
-    if (w >= TileStateIO<typename CarryTraits<S, Op>::C>::STRIDE && w <= a.state_stride) a.state_stride = w;
-  }
-  // The TMA tile kernels are instantiated only for power-of-two element sizes
+                          static_cast<uint32_t*>(ws), 0u, 0u, scan_lookback_mode(), nullptr,
+                          scan_backoff_ns(), relax_epoch ? 0u : 0x3fffffffu};
+  // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
   if constexpr (smem_scan_type_ok<T>()) {
-  CUtensorMap tmap;
-  const bool smem = !scan_force_regs() && src_stride == 1 && dst_stride == 1 && n >= WsT::kTileSmem &&
-                    make_rows128_map(&tmap, src, (n * sizeof(T)) / kRowBytes, uint32_t(kScanThreads));
-  if (smem) {
-    a.ntiles = uint32_t(ceil_div(n, WsT::kTileSmem));
-    CUtensorMap tmap_out = tmap;
-    const bool tstore = sizeof(S) == sizeof(T) && !scan_env_u32("FORGE_SCAN_NO_TMA_STORE", 0) &&
-                        make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
-#ifdef FORGE_SCAN_EXPERIMENTS
-    // Measured alternatives, built only with
-    // `make EXPERIMENTS=1`: FORGE_SCAN_PATH=chain|ws|pipe, FORGE_SCAN_CLUSTER=K.
-    if (scan_path() == 3) {
-      const cudaError_t e = inclusive ? launch_scan_chain<T, S, F, Op, true>(a, tmap, tmap_out, tstore, stream)
-                                      : launch_scan_chain<T, S, F, Op, false>(a, tmap, tmap_out, tstore, stream);
-      return e != cudaSuccess ? e : cudaGetLastError();
-    }
-    const uint32_t K = scan_cluster_size();
-    if (scan_path() == 0 && K > 1) {
-      const uint32_t nsub = a.ntiles;
-      a.ntiles = uint32_t(ceil_div(nsub, K));  // look-back tiles = clusters
-      const cudaError_t e =
-          inclusive ? launch_scan_cluster<T, S, F, Op, true>(a, tmap, tmap_out, tstore, K, nsub, stream)
-                    : launch_scan_cluster<T, S, F, Op, false>(a, tmap, tmap_out, tstore, K, nsub, stream);
-      return e != cudaSuccess ? e : cudaGetLastError();
-    }
-    if (scan_path() == 2) {
-      if (inclusive) {
-        const uint32_t g = scan_ws_grid<T, S, F, Op, true>(a.ntiles);
-        scan_ws_kernel<T, S, F, Op, true>
-            <<<g, kWsThreads, ws_dyn_bytes<T, S, Op>(), stream>>>(a, tmap, tmap_out, tstore);
-      } else {
-        const uint32_t g = scan_ws_grid<T, S, F, Op, false>(a.ntiles);
-        scan_ws_kernel<T, S, F, Op, false>
-            <<<g, kWsThreads, ws_dyn_bytes<T, S, Op>(), stream>>>(a, tmap, tmap_out, tstore);
-      }
-      return cudaGetLastError();
-    }
-    if (!scan_use_one_tile_kernel()) {
-      if (inclusive) {
-        const uint32_t g = scan_pipe_grid<T, S, F, Op, true>(a.ntiles);
-        scan_pipe_kernel<T, S, F, Op, true><<<g, kPipeThreads, kPipeDyn, stream>>>(a, tmap, tmap_out, tstore);
-      } else {
-        const uint32_t g = scan_pipe_grid<T, S, F, Op, false>(a.ntiles);
-        scan_pipe_kernel<T, S, F, Op, false><<<g, kPipeThreads, kPipeDyn, stream>>>(a, tmap, tmap_out, tstore);
-      }
-      return cudaGetLastError();
-    }
+    constexpr int R = scan_subtiles<T>();
+    constexpr uint64_t kTile = uint64_t(R) * kScanThreads * smem_scan_items<T>();
+    CUtensorMap tmap;
+    const bool smem = !scan_force_regs() && src_stride == 1 && dst_stride == 1 && n >= kTile &&
+                      make_rows128_map(&tmap, src, (n * sizeof(T)) / kRowBytes, uint32_t(kScanThreads));
+    if (smem) {
+      a.ntiles = uint32_t(ceil_div(n, kTile));
+      a.state_stride = WsT::slot_words(a.ntiles, ws_bytes);
+      if (a.state_stride == 0) return cudaErrorInvalidValue;
+#ifdef FORGE_DEV
+      a.trace = scan_trace_for(a.ntiles);
 #endif
-    if constexpr (sizeof(T) >= 16) {
-      if (scan_subtiles<T>() == 2) {
-        a.ntiles = uint32_t(ceil_div(n, 2 * WsT::kTileSmem));
-        return inclusive ? launch_scan_smem<T, S, F, Op, true, 2>(a, tmap, tmap_out, tstore, stream)
-                         : launch_scan_smem<T, S, F, Op, false, 2>(a, tmap, tmap_out, tstore, stream);
-      }
+      if (const cudaError_t e = ws_claim(ws, kWsTagScan, 256 + uint64_t(a.ntiles) * a.state_stride * 8, stream);
+          e != cudaSuccess)
+        return e;
+      CUtensorMap tmap_out = tmap;
+      const bool tstore = sizeof(S) == sizeof(T) && !scan_no_tma_store() &&
+                          make_rows128_map(&tmap_out, dst, (n * sizeof(S)) / kRowBytes, uint32_t(kScanThreads));
+      return inclusive ? launch_scan_smem<T, S, F, Op, true, R>(a, tmap, tmap_out, tstore, stream)
+                       : launch_scan_smem<T, S, F, Op, false, R>(a, tmap, tmap_out, tstore, stream);
     }
-    return inclusive ? launch_scan_smem<T, S, F, Op, true, 1>(a, tmap, tmap_out, tstore, stream)
-                     : launch_scan_smem<T, S, F, Op, false, 1>(a, tmap, tmap_out, tstore, stream);
-  }
   }
   a.ntiles = uint32_t(ceil_div(n, WsT::kTileGeneral));
+  a.state_stride = WsT::slot_words(a.ntiles, ws_bytes);
+  if (a.state_stride == 0) return cudaErrorInvalidValue;
+  if (const cudaError_t e = ws_claim(ws, kWsTagScan, 256 + uint64_t(a.ntiles) * a.state_stride * 8, stream);
+      e != cudaSuccess)
+    return e;
   if (inclusive)
     scan_kernel<T, S, F, Op, true><<<a.ntiles, kScanThreads, 0, stream>>>(a);
   else

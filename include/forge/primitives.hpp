@@ -22,12 +22,18 @@
 //   * The geometry fields of ArchParams are validated like the reference but
 //     the kernels choose their own tiles / grids; RunOptions::backend,
 //     schedule and tuning are accepted and ignored (there is no simulator and
-//     no CPU fallback); mutate is ignored.
+//     no CPU fallback).  mutate.relax_scan_flag selects the scan ablation (tile
+//     states of earlier launches accepted: a broken publication protocol the
+//     stress tests must catch); relax_mapreduce_flag is accepted and ignored
+//     (the mapreduce never waits on another block's flag).
 //   * Workspaces use the B200 layouts (forge/cuda/*.cuh): they are zeroed once
-//     at creation and self-reset, so no fill_zero happens per launch.
+//     at creation and self-reset, so no fill_zero happens per launch; a
+//     workspace moved to another layout (another primitive, another matrix
+//     plan) is re-zeroed by the library first (cuda::ws_claim).
 #pragma once
 
 #include <algorithm>
+#include <cstddef>
 #include <optional>
 #include <span>
 #include <vector>
@@ -192,26 +198,81 @@ inline uint64_t scan_tiles(uint64_t n, const ArchParams& p) {
   return (n + tile - 1) / tile;
 }
 
+// Matrix primitive geometry (primitives.hpp:202-244), kept for the API: the
+// same fields and the reference's own formulas, so code that sizes or logs a
+// plan keeps compiling and gets the same numbers.  The sm_100a kernels plan
+// their own launches; b200_plan_mat<T>() (nvcc TUs) reports that geometry in
+// the same struct.
+struct MatPlan {
+  bool wide = false;
+  uint64_t nb = 1;            // tall: slices per output (B200: row / column splits)
+  uint64_t rows_per_slice = 0;
+  uint64_t grid_outputs = 0;  // tall: outputs in flight
+  uint64_t groups = 0;        // wide: output groups per grid pass
+  LaunchConfig cfg;
+  uint64_t slots = 0;         // partial slots (nb > 1)
+};
+
+inline uint64_t tall_slices(uint64_t reduce_len, const ArchParams& p) {
+  const uint64_t per_slice = uint64_t(p.threads_per_block) * p.nitem_copy * 8;
+  return std::clamp<uint64_t>((reduce_len + per_slice - 1) / per_slice, 1, p.mapreduce_blocks);
+}
+
+inline MatPlan plan_mat(uint64_t reduce_len, uint64_t outputs, bool commutative, const ArchParams& params) {
+  const ArchParams p = params.normalized();
+  MatPlan plan;
+  const uint32_t V = p.nitem_copy;
+  const bool order_free = commutative || reduce_len <= V;
+  if (outputs >= p.matvec_wide_min_outputs && order_free) {
+    plan.wide = true;
+    const uint32_t warps = p.matvec_wide_block_threads / p.warp_width;
+    const uint64_t per_block = uint64_t(warps) * p.matvec_wide_warp_cols;
+    const uint64_t needed = (outputs + per_block - 1) / per_block;
+    plan.groups = needed;
+    plan.cfg.num_blocks = uint32_t(std::min<uint64_t>(needed, 2ull * p.mapreduce_blocks));
+    plan.cfg.threads_per_block = p.matvec_wide_block_threads;
+  } else {
+    plan.nb = tall_slices(reduce_len, p);
+    plan.rows_per_slice = (reduce_len + plan.nb - 1) / plan.nb;
+    plan.grid_outputs = std::min<uint64_t>(outputs, std::max<uint64_t>(1, 4ull * p.mapreduce_blocks / plan.nb));
+    plan.cfg.num_blocks = uint32_t(plan.nb * plan.grid_outputs);
+    plan.cfg.threads_per_block = p.threads_per_block;
+    if (plan.nb > 1) plan.slots = plan.nb * outputs;
+  }
+  plan.cfg.warp_width = p.warp_width;
+  return plan;
+}
+
 namespace detail {
 
 inline uint64_t rup(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
-// Scan tile of the B200 kernels for an S of `s_size` bytes (cuda::scan_items).
-inline uint64_t b200_scan_tile(uint32_t s_size) {
-  uint64_t it = 64 / std::max<uint32_t>(s_size, 1);
-  it = std::clamp<uint64_t>(it, 1, 16);
-  return 256 * it;
+// Scan workspace bound for an S of `s_size` bytes (cuda::ScanWs, which this
+// mirrors with the carry bounded by 2 * sizeof(S): f32 sums carry in f64):
+// the smem kernel's tiles of a sizeof(S)-byte T at full 256-byte slots, or the
+// general kernel's tiles (256 x 64 bytes of S) at packed slots, whichever is
+// larger.  Smaller workspaces (down to packed slots) are accepted too.
+inline uint64_t b200_scan_general_tile(uint32_t s_size) {
+  return 256 * std::clamp<uint64_t>(64 / std::max<uint32_t>(s_size, 1), 1, 16);
 }
-// State bytes per tile when the carry is up to 2x the accumulator (f32 sums carry in f64).
-inline uint64_t b200_state_bytes(uint32_t accum_size) {
+inline uint64_t b200_scan_sized_tile(uint32_t s_size) {
+  if (s_size >= 16) return 2 * 256 * 8;
+  return 256 * std::max<uint64_t>(128 / std::max<uint32_t>(s_size, 1), 1);
+}
+inline uint64_t b200_state_min_bytes(uint32_t accum_size) {  // packed slot: every 32-bit chunk of the carry
   const uint64_t words = (2ull * accum_size + 3) / 4;
   uint64_t stride = 1;
   while (stride < words) stride <<= 1;
-  return std::max<uint64_t>(stride * 8, 256);  // 256-byte slot per tile (cuda::kStateSlotWords)
+  return stride * 8;
 }
 inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
-  const uint64_t tiles = (n + b200_scan_tile(accum_size) - 1) / b200_scan_tile(accum_size);
-  return 256 + std::max<uint64_t>(tiles, 1) * b200_state_bytes(accum_size);
+  const uint64_t full = 256 + std::max<uint64_t>((n + b200_scan_sized_tile(accum_size) - 1) /
+                                                     b200_scan_sized_tile(accum_size), 1) *
+                                  std::max<uint64_t>(b200_state_min_bytes(accum_size), 256);
+  const uint64_t packed = 256 + std::max<uint64_t>((n + b200_scan_general_tile(accum_size) - 1) /
+                                                       b200_scan_general_tile(accum_size), 1) *
+                                    b200_state_min_bytes(accum_size);
+  return std::max(full, packed);
 }
 inline uint64_t b200_sm_count() {
   int dev = 0, sms = 0;
@@ -271,7 +332,7 @@ Workspace make_scan_workspace(Machine& m, uint64_t n, const ArchParams& params) 
   (void)params.normalized();
   Workspace ws;
   const uint64_t bytes = detail::b200_scan_ws_bytes(n, sizeof(S));
-  ws.tiles = (bytes - 256) / detail::b200_state_bytes(sizeof(S));
+  ws.tiles = (n + detail::b200_scan_general_tile(sizeof(S)) - 1) / detail::b200_scan_general_tile(sizeof(S));
   ws.tile_flag = intr::create_buffer<uint8_t>(m, bytes, 256);
   return ws;
 }
@@ -298,6 +359,39 @@ Workspace make_mat_workspace(Machine& m, uint64_t reduce_len, uint64_t outputs,
 }
 
 #ifdef __CUDACC__
+
+// The geometry the sm_100a kernels actually launch for matvec (gevm, fold down
+// the n rows of each of p columns) or vecmat (gemv, fold across the p columns
+// of each of n rows), in the reference's MatPlan terms: `wide` = the
+// column-group / row-per-thread kernels (commutative ops on aligned data), `nb`
+// = splits of the fold per output, `slots` = partials in the workspace.
+template <class T>
+MatPlan b200_plan_mat(Primitive prim, uint64_t n, uint64_t p_cols, bool commutative) {
+  MatPlan plan;
+  plan.cfg.warp_width = 32;
+  plan.cfg.threads_per_block = cuda::kMatThreads;
+  if (prim == Primitive::VecMat) {
+    const cuda::GemvPlan g = cuda::plan_gemv<T>(n, p_cols);
+    plan.wide = true;
+    plan.nb = g.ks;
+    plan.rows_per_slice = g.cols_per_split;
+    plan.groups = g.row_blocks;
+    plan.grid_outputs = n;
+    plan.cfg.num_blocks = uint32_t(g.grid);
+    plan.slots = g.ks > 1 ? g.ks * n : 0;
+    return plan;
+  }
+  const bool cols = commutative && cuda::gevm_cols_enabled();
+  const cuda::GevmPlan g = cols ? cuda::plan_gevm_cols<T>(n, p_cols) : cuda::plan_gevm<T>(n, p_cols);
+  plan.wide = cols;
+  plan.nb = g.ks;
+  plan.rows_per_slice = g.rows_per_split;
+  plan.groups = cols ? cuda::ceil_div(p_cols, cuda::kGevmCols) : p_cols;
+  plan.grid_outputs = p_cols;
+  plan.cfg.num_blocks = uint32_t(g.grid);
+  plan.slots = g.ks > 1 ? g.ks * p_cols : 0;
+  return plan;
+}
 
 namespace detail {
 
@@ -412,7 +506,7 @@ LaunchReport mapreduce(Machine& m, const SemiringSpec<F, S, Op>& spec, View<T> s
   }
   if (ws.partials < 0 || ws.result < 0 ||
       detail::buffer_bytes(m, ws.partials) < detail::b200_mapreduce_ws_bytes(sizeof(S)) ||
-      detail::buffer_bytes(m, ws.result) < sizeof(S) + 4)
+      detail::buffer_bytes(m, ws.result) < detail::rup(sizeof(S), 16) + sizeof(uint32_t))
     raise(ErrorCode::WorkspaceTooSmall, "mapreduce workspace");
   const T* sp = intr::view_ptr(m, src);
   char* wsp = static_cast<char*>(m.device_ptr(ws.partials));
@@ -449,7 +543,8 @@ LaunchReport scan(Machine& m, const SemiringSpec<F, S, Op>& spec, View<T> src, V
     return rep;
   }
   using WsT = cuda::ScanWs<T, S, Op>;
-  if (ws.tile_flag < 0 || detail::buffer_bytes(m, ws.tile_flag) < WsT::bytes(n))
+  const uint64_t ws_bytes = detail::buffer_bytes(m, ws.tile_flag);
+  if (ws.tile_flag < 0 || ws_bytes < WsT::min_bytes_for(cuda::ceil_div(n, WsT::kTileGeneral)))
     raise(ErrorCode::WorkspaceTooSmall, "scan workspace");
   const T* sp = intr::view_ptr(m, src);
   S* dp = intr::view_ptr(m, dst);
@@ -457,8 +552,9 @@ LaunchReport scan(Machine& m, const SemiringSpec<F, S, Op>& spec, View<T> src, V
   const S ident = spec.identity.value_or(S{});
   LaunchReport rep = detail::run_timed(m, opt, "scan", n, [&](uint64_t& k) {
     k = 1;
-    return cuda::launch_scan<T, S, F, Op>(sp, src.stride, dp, dst.stride, n, inclusive, spec.map,
-                                          spec.op, ident, nullptr, nullptr, wsp, m.stream());
+    return cuda::launch_scan<T, S, F, Op>(sp, src.stride, dp, dst.stride, n, inclusive, spec.map, spec.op, ident,
+                                          nullptr, nullptr, wsp, ws_bytes, m.stream(),
+                                          opt.mutate.relax_scan_flag);
   });
   detail::count_load(rep, src.buf, n);
   detail::count_store(rep, dst.buf, n);
@@ -584,3 +680,20 @@ LaunchReport mapreduce_2d(Machine& m, const SemiringSpec<F, S, Op>& spec, View<T
 #endif  // __CUDACC__
 
 }  // namespace forge::prim
+
+namespace forge::intr {
+
+// Descriptor of OptVal<S> (primitives.hpp:840-853): the value at 0, the valid
+// byte after it, the C++ size (padding included).
+template <class S>
+struct TypeOf<prim::OptVal<S>> {
+  static const TypeDescriptor& get() {
+    static const TypeDescriptor d = TypeDescriptor::struct_of(
+        {{descriptor_of<S>(), 0},
+         {TypeDescriptor::primitive(Scalar::U8), uint32_t(offsetof(prim::OptVal<S>, valid))}},
+        uint32_t(sizeof(prim::OptVal<S>)));
+    return d;
+  }
+};
+
+}  // namespace forge::intr

@@ -53,6 +53,30 @@ uint8_t orc_uf8_encode(float x) { /* algebra.hpp:22-28: nearest, ties to even */
   return (uint8_t)nearbyintf(scaled);
 }
 
+/* variant 2 of the f32 ops: special values for the order-independence tests
+ * of max / min / argmax (about 1 in 2^15 elements a NaN with a random payload
+ * and sign, 1 in 2^15 an infinity, 1/8 a signed zero, 1/16 a small integer,
+ * the rest gen_f32_sym).  Mirrored bit for bit by capi.cu's fill_kernel. */
+static float gen_f32_special(uint64_t u) {
+  const uint32_t low = (uint32_t)(u & 0xFFFFu);
+  uint32_t bits;
+  float f;
+  if (low < 2u) {
+    bits = 0x7fc00000u | (uint32_t)((u >> 16) & 0x3FFFFFu) | (low ? 0x80000000u : 0u);
+  } else if (low < 4u) {
+    bits = low == 2u ? 0x7f800000u : 0xff800000u;
+  } else if (low < 0x2000u) {
+    bits = (u >> 16) & 1u ? 0x80000000u : 0u;
+  } else if (low < 0x3000u) {
+    f = (float)(int32_t)((u >> 16) & 7u) - 4.0f;
+    return f;
+  } else {
+    return gen_f32_sym(u);
+  }
+  memcpy(&f, &bits, 4);
+  return f;
+}
+
 static void gen_one(forge_op op, uint64_t u, uint64_t idx, int32_t variant, unsigned char* out) {
   switch (op) {
     case FORGE_OP_F32_SUM:
@@ -63,7 +87,7 @@ static void gen_one(forge_op op, uint64_t u, uint64_t idx, int32_t variant, unsi
     case FORGE_OP_MV_F32_PLUS_TIMES:
     case FORGE_OP_MV_F32_MIN_PLUS:
     case FORGE_OP_MV_F32_MAX_PLUS: {
-      float v = variant == 1 ? gen_f32_pos(u) : gen_f32_sym(u);
+      float v = variant == 1 ? gen_f32_pos(u) : variant == 2 ? gen_f32_special(u) : gen_f32_sym(u);
       memcpy(out, &v, 4);
       break;
     }
@@ -96,7 +120,7 @@ static void gen_one(forge_op op, uint64_t u, uint64_t idx, int32_t variant, unsi
     }
     case FORGE_OP_ARGMAX_F32I32: {
       forge_argmax v;
-      v.v = variant == 1 ? (float)(int32_t)((u >> 60) & 0xF) : gen_f32_sym(u);
+      v.v = variant == 1 ? (float)(int32_t)((u >> 60) & 0xF) : variant == 2 ? gen_f32_special(u) : gen_f32_sym(u);
       v.i = (int32_t)(uint32_t)idx;
       memcpy(out, &v, 8);
       break;
@@ -213,9 +237,36 @@ static forge_mat2_u32 mat2_mul(forge_mat2_u32 a, forge_mat2_u32 b) { /* algebra.
   return r;
 }
 
+/* Order-independent f32 max / min (include/forge/algebra.hpp fmax_total):
+ * NaN -> canonical quiet NaN, -0 < +0.  Equal to the reference's
+ * `a >= b ? a : b` (algebra ops of SPEC.md) on NaN-free inputs without
+ * zero-sign ties, where that operator is itself order-dependent. */
+static float canonical_nan(void) {
+  const uint32_t bits = 0x7fc00000u;
+  float f;
+  memcpy(&f, &bits, 4);
+  return f;
+}
+static float fmax_total(float a, float b) {
+  if (a != a || b != b) return canonical_nan();
+  if (a == b) return signbit(a) ? b : a;
+  return a > b ? a : b;
+}
+static float fmin_total(float a, float b) {
+  if (a != a || b != b) return canonical_nan();
+  if (a == b) return signbit(a) ? a : b;
+  return a < b ? a : b;
+}
+
+/* ArgMax (new BASELINE C3 type): max by v, ties to the smaller i; NaN ranks
+ * above every number, so the op stays associative with NaN inputs. */
 static forge_argmax argmax_op(forge_argmax a, forge_argmax b) {
-  if (a.v > b.v) return a;
-  if (b.v > a.v) return b;
+  const int an = a.v != a.v, bn = b.v != b.v;
+  if (an != bn) return an ? a : b;
+  if (!an) {
+    if (a.v > b.v) return a;
+    if (b.v > a.v) return b;
+  }
   return a.i <= b.i ? a : b;
 }
 
@@ -275,13 +326,11 @@ static sval combine_exact(forge_op op, sval a, sval b) {
   switch (op) {
     case FORGE_OP_F32_MAX:
     case FORGE_OP_MV_F32_MAX_PLUS:
-      r.f = a.f >= b.f ? a.f : b.f;
-      if (a.f != a.f || b.f != b.f) r.f = NAN;
+      r.f = fmax_total(a.f, b.f);
       break;
     case FORGE_OP_F32_MIN:
     case FORGE_OP_MV_F32_MIN_PLUS:
-      r.f = a.f <= b.f ? a.f : b.f;
-      if (a.f != a.f || b.f != b.f) r.f = NAN;
+      r.f = fmin_total(a.f, b.f);
       break;
     case FORGE_OP_I32_SUM:
     case FORGE_OP_U32_SUM:

@@ -12,7 +12,10 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libforge.so"
+# FORGE_LIB=dev selects libforge_dev.so (`make DEV=1`: the same kernels plus the
+# environment-read development knobs); the product is libforge.so.
+LIB_PATH = Path(__file__).resolve().parent / ("libforge_dev.so" if os.environ.get("FORGE_LIB") == "dev"
+                                              else "libforge.so")
 
 # ---- status codes (forge_status) ------------------------------------------
 OK = 0
@@ -128,6 +131,7 @@ _SIGNATURES = {
     "forge_mapreduce_2d": (C.c_int, [_P, Semiring, View, _u64, _u64, C.c_int, View, C.POINTER(Workspace),
                                      C.POINTER(ArchParams), C.POINTER(LaunchReport)]),
     "forge_vcopy": (C.c_int, [_P, View, View, _u32, C.POINTER(ArchParams), C.POINTER(LaunchReport)]),
+    "forge_set_mutation_flags": (C.c_int, [_i32, _i32]),
     "forge_vload_pattern": (C.c_int, [_u64, _u32, C.POINTER(_u32), C.POINTER(_u32)]),
     "forge_dev_workspace_bytes": (C.c_int, [C.c_int, C.c_int, _u64, _u64, C.POINTER(_u64)]),
     "forge_dev_mapreduce": (C.c_int, [C.c_int, _P, _u64, _P, _P, _u64, _P]),

@@ -1,133 +1,8 @@
-// capi.cu — the extern "C" surface of include/forge.h over the forge::prim
-// templates and the sm_100a kernels (the `capi.cpp` that
-// /root/reference/proj/src/CMakeLists.txt:13-17 declares but never ships).
-//
-// Every entry point: exceptions never cross the boundary.  forge::Error ->
-// 1 + ErrorCode; forge::NoDeviceError -> FORGE_ERR_NO_DEVICE; a CUDA failure
-// -> FORGE_ERR_DEVICE_FAULT (and LaunchReport{ok = 0} when a report is passed).
-#include <cstring>
-#include <string>
-
-#include "forge.h"
-#include "forge/bitstype.hpp"
-#include "menu.cuh"
-
-using namespace forge;
-using forge::prim::ArchParams;
-using forge::prim::Workspace;
-
-namespace {
-
-thread_local std::string g_last_error;
-
-void set_error(const std::string& s) { g_last_error = s; }
-
-template <class Fn>
-int guarded(Fn&& fn) {
-  try {
-    const int rc = fn();
-    if (rc == FORGE_OK) g_last_error.clear();
-    return rc;
-  } catch (const forge::Error& e) {
-    set_error(std::string(to_string(e.code())) + ": " + e.what());
-    return e.status();
-  } catch (const forge::NoDeviceError& e) {
-    set_error(e.what());
-    return FORGE_ERR_NO_DEVICE;
-  } catch (const std::exception& e) {
-    set_error(e.what());
-    return FORGE_ERR_DEVICE_FAULT;
-  }
-}
-
-int unsupported_op(forge_op op, const char* what) {
-  set_error(std::string("Unsupported: op ") + std::to_string(int(op)) + " is not in the " + what +
-            " menu");
-  return FORGE_ERR_UNSUPPORTED;
-}
-
-ArchParams to_params(const forge_arch_params* p) {
-  ArchParams a;
-  if (p) {
-    a.warp_width = p->warp_width;
-    a.mapreduce_blocks = p->mapreduce_blocks;
-    a.threads_per_block = p->threads_per_block;
-    a.nitem_scan = p->nitem_scan;
-    a.nitem_copy = p->nitem_copy;
-    a.lookback_window = p->lookback_window;
-    a.matvec_wide_warp_cols = p->matvec_wide_warp_cols;
-    a.matvec_wide_block_threads = p->matvec_wide_block_threads;
-    a.matvec_wide_min_outputs = p->matvec_wide_min_outputs;
-  }
-  return a;
-}
-
-Workspace from_c(const forge_workspace* w) {
-  Workspace r;
-  if (!w) return r;
-  r.tile_aggregate = w->tile_aggregate;
-  r.tile_prefix = w->tile_prefix;
-  r.tile_flag = w->tile_flag;
-  r.partials = w->partials;
-  r.flags = w->flags;
-  r.result = w->result;
-  r.tiles = w->tiles;
-  r.slots = w->slots;
-  return r;
-}
-
-void to_c(const Workspace& r, forge_workspace* w) {
-  w->tile_aggregate = r.tile_aggregate;
-  w->tile_prefix = r.tile_prefix;
-  w->tile_flag = r.tile_flag;
-  w->partials = r.partials;
-  w->flags = r.flags;
-  w->result = r.result;
-  w->tiles = r.tiles;
-  w->slots = r.slots;
-}
-
-int finish(const LaunchReport& r, forge_launch_report* out) {
-  if (out) {
-    out->ok = r.ok ? 1 : 0;
-    out->fault_kind = int32_t(r.fault.kind);
-    out->steps = r.steps;
-    out->wall_seconds = r.wall_seconds;
-    std::memset(out->detail, 0, sizeof(out->detail));
-    std::strncpy(out->detail, r.fault.detail.c_str(), sizeof(out->detail) - 1);
-  }
-  if (!r.ok) {
-    set_error("device fault: " + r.fault.detail);
-    return FORGE_ERR_DEVICE_FAULT;
-  }
-  return FORGE_OK;
-}
-
-template <class T>
-intr::View<T> view_of(const forge_view& v) {
-  return intr::View<T>{v.buf, v.offset, v.length, v.stride == 0 ? 1 : v.stride};
-}
-
-int from_cuda(cudaError_t e, const char* what) {
-  if (e == cudaSuccess) return FORGE_OK;
-  set_error(std::string(what) + ": " + cudaGetErrorString(e));
-  return FORGE_ERR_DEVICE_FAULT;
-}
-
-int require_ws(uint64_t have, uint64_t need, const char* what) {
-  if (have < need) {
-    set_error(std::string("WorkspaceTooSmall: ") + what + " needs " + std::to_string(need) +
-              " bytes, got " + std::to_string(have));
-    return FORGE_ERR_WORKSPACE_TOO_SMALL;
-  }
-  return FORGE_OK;
-}
-
-}  // namespace
-
-struct forge_machine {
-  Machine m;
-};
+// capi.cu — the extern "C" surface of include/forge.h (core: machine, buffers,
+// descriptors, workspaces, vcopy, synthetic data, copy).  The primitive entry
+// points live in capi_scan.cu, capi_reduce.cu and capi_matrix.cu so the
+// menu's kernel instantiations compile in parallel.
+#include "capi_common.cuh"
 
 // ---------------------------------------------------------------------------
 // Synthetic data on the device (bit-identical to oracle/oracle.c gen_one).
@@ -144,6 +19,16 @@ __device__ __forceinline__ float dsym(uint64_t u) {
   return __fadd_rn(__fmul_rn(float(int32_t(u >> 40)), 0x1p-23f), -1.0f);
 }
 __device__ __forceinline__ float dpos(uint64_t u) { return __fmul_rn(float(int32_t(u >> 40)), 0x1p-24f); }
+// variant 2: NaN (random payload and sign) / +-inf / signed zeros / small
+// integers among ordinary values — oracle.c gen_f32_special, bit for bit.
+__device__ __forceinline__ float dspecial(uint64_t u) {
+  const uint32_t low = uint32_t(u & 0xFFFFu);
+  if (low < 2u) return __uint_as_float(0x7fc00000u | uint32_t((u >> 16) & 0x3FFFFFu) | (low ? 0x80000000u : 0u));
+  if (low < 4u) return __uint_as_float(low == 2u ? 0x7f800000u : 0xff800000u);
+  if (low < 0x2000u) return __uint_as_float((u >> 16) & 1u ? 0x80000000u : 0u);
+  if (low < 0x3000u) return __fadd_rn(float(int32_t((u >> 16) & 7u)), -4.0f);
+  return dsym(u);
+}
 
 __global__ void fill_kernel(int op, unsigned char* dst, uint64_t n, uint64_t seed, uint64_t base,
                             int variant) {
@@ -155,7 +40,7 @@ __global__ void fill_kernel(int op, unsigned char* dst, uint64_t n, uint64_t see
       case FORGE_OP_F32_SUM: case FORGE_OP_F32_SUMSQ: case FORGE_OP_F32_MAX: case FORGE_OP_F32_MIN:
       case FORGE_OP_F32_LOGSUMEXP: case FORGE_OP_MV_F32_PLUS_TIMES: case FORGE_OP_MV_F32_MIN_PLUS:
       case FORGE_OP_MV_F32_MAX_PLUS:
-        reinterpret_cast<float*>(dst)[i] = variant == 1 ? dpos(u) : dsym(u);
+        reinterpret_cast<float*>(dst)[i] = variant == 1 ? dpos(u) : variant == 2 ? dspecial(u) : dsym(u);
         break;
       case FORGE_OP_F64_SUM: case FORGE_OP_MV_F64_PLUS_TIMES:
         reinterpret_cast<double*>(dst)[i] = __dadd_rn(__dmul_rn(double(int64_t(u >> 11)), 0x1p-52), -1.0);
@@ -179,7 +64,7 @@ __global__ void fill_kernel(int op, unsigned char* dst, uint64_t n, uint64_t see
       }
       case FORGE_OP_ARGMAX_F32I32: {
         forge::alg::ArgMax v;
-        v.v = variant == 1 ? float(int32_t((u >> 60) & 0xF)) : dsym(u);
+        v.v = variant == 1 ? float(int32_t((u >> 60) & 0xF)) : variant == 2 ? dspecial(u) : dsym(u);
         v.i = int32_t(uint32_t(idx));
         reinterpret_cast<forge::alg::ArgMax*>(dst)[i] = v;
         break;
@@ -439,83 +324,23 @@ int forge_workspace_release(forge_machine* m, forge_workspace* ws) {
 
 // ---- primitives ------------------------------------------------------------
 
-int forge_scan(forge_machine* m, forge_semiring spec, forge_view src, forge_view dst,
-               int32_t inclusive, forge_workspace* ws, const forge_arch_params* params,
-               forge_launch_report* report) {
-  return guarded([&]() -> int {
-    Workspace w = from_c(ws);
-    int rc = menu::visit1(spec.op, [&](auto e) {
-      using E = decltype(e);
-      LaunchReport r = prim::scan(m->m, e.spec(spec.has_identity != 0), view_of<typename E::T>(src),
-                                  view_of<typename E::S>(dst), inclusive != 0, w, to_params(params));
-      return finish(r, report);
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(spec.op, "scan") : rc;
-  });
+int forge_set_mutation_flags(int32_t relax_scan_flag, int32_t relax_mapreduce_flag) {
+  g_mutate.relax_scan_flag = relax_scan_flag != 0;
+  g_mutate.relax_mapreduce_flag = relax_mapreduce_flag != 0;
+  return FORGE_OK;
 }
 
-int forge_mapreduce(forge_machine* m, forge_semiring spec, forge_view src, forge_workspace* ws,
-                    const forge_arch_params* params, void* out_host, forge_launch_report* report) {
-  return guarded([&]() -> int {
-    Workspace w = from_c(ws);
-    int rc = menu::visit1(spec.op, [&](auto e) {
-      using E = decltype(e);
-      typename E::S r{};
-      LaunchReport rep = prim::mapreduce(m->m, e.spec(spec.has_identity != 0), view_of<typename E::T>(src), w,
-                                         to_params(params), &r);
-      if (rep.ok) std::memcpy(out_host, &r, sizeof(r));
-      return finish(rep, report);
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(spec.op, "mapreduce") : rc;
-  });
-}
 
-int forge_matvec(forge_machine* m, forge_semiring spec, forge_view A, uint64_t n, uint64_t p_cols,
-                 forge_view x, forge_view y, forge_workspace* ws, const forge_arch_params* params,
-                 forge_launch_report* report, int32_t uses_vector) {
-  return guarded([&]() -> int {
-    Workspace w = from_c(ws);
-    int rc = menu::visit2(spec.op, [&](auto e) {
-      using E = decltype(e);
-      LaunchReport r = prim::matvec<typename E::T, typename E::S>(
-          m->m, e.spec(spec.has_identity != 0), view_of<typename E::T>(A), n, p_cols,
-          view_of<typename E::T>(x), view_of<typename E::S>(y), w, to_params(params), {}, uses_vector != 0);
-      return finish(r, report);
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(spec.op, "matrix") : rc;
-  });
-}
 
-int forge_vecmat(forge_machine* m, forge_semiring spec, forge_view A, uint64_t n, uint64_t p_cols,
-                 forge_view x, forge_view z, forge_workspace* ws, const forge_arch_params* params,
-                 forge_launch_report* report, int32_t uses_vector) {
-  return guarded([&]() -> int {
-    Workspace w = from_c(ws);
-    int rc = menu::visit2(spec.op, [&](auto e) {
-      using E = decltype(e);
-      LaunchReport r = prim::vecmat<typename E::T, typename E::S>(
-          m->m, e.spec(spec.has_identity != 0), view_of<typename E::T>(A), n, p_cols,
-          view_of<typename E::T>(x), view_of<typename E::S>(z), w, to_params(params), {}, uses_vector != 0);
-      return finish(r, report);
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(spec.op, "matrix") : rc;
-  });
-}
+
+
 
 int forge_mapreduce_2d(forge_machine* m, forge_semiring spec, forge_view A, uint64_t n, uint64_t p_cols,
                        forge_reduce_axis axis, forge_view out, forge_workspace* ws,
                        const forge_arch_params* params, forge_launch_report* report) {
   return guarded([&]() -> int {
-    Workspace w = from_c(ws);
-    int rc = menu::visit1(spec.op, [&](auto e) {
-      using E = decltype(e);
-      LaunchReport r = prim::mapreduce_2d<typename E::T, typename E::S>(
-          m->m, e.spec(spec.has_identity != 0), view_of<typename E::T>(A), n, p_cols,
-          axis == FORGE_AXIS_ROWS ? prim::ReduceAxis::Rows : prim::ReduceAxis::Cols,
-          view_of<typename E::S>(out), w, to_params(params));
-      return finish(r, report);
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(spec.op, "mapreduce_2d") : rc;
+    return axis == FORGE_AXIS_ROWS ? mapreduce_2d_rows(m, spec, A, n, p_cols, out, ws, params, report)
+                                   : mapreduce_2d_cols(m, spec, A, n, p_cols, out, ws, params, report);
   });
 }
 
@@ -620,141 +445,11 @@ int forge_dev_workspace_bytes(forge_primitive prim, forge_op op, uint64_t n, uin
   });
 }
 
-int forge_dev_mapreduce(forge_op op, const void* src, uint64_t n, void* out_dev, void* ws,
-                        uint64_t ws_bytes, void* stream) {
-  forge::prim::detail::NvtxRange nvtx_range("forge_dev_mapreduce");
-  return guarded([&]() -> int {
-    int rc = menu::visit1(op, [&](auto e) -> int {
-      using E = decltype(e);
-      using T = typename E::T;
-      using S = typename E::S;
-      cudaStream_t st = static_cast<cudaStream_t>(stream);
-      if (!e.commutative) {
-        set_error("InvalidArgument: mapreduce requires a commutative op; use forge_dev_reduce_ordered");
-        return FORGE_ERR_INVALID_ARGUMENT;
-      }
-      if (n == 0)
-        return from_cuda(cudaMemcpyAsync(out_dev, &e.identity, sizeof(S), cudaMemcpyHostToDevice, st),
-                         "identity copy");
-      int w = require_ws(ws_bytes, cuda::MapReduceWs<S>::bytes(cuda::mapreduce_max_grid()), "mapreduce");
-      if (w) return w;
-      return from_cuda(cuda::launch_mapreduce<T, S>(static_cast<const T*>(src), n, 1, typename E::F{},
-                                                    typename E::Op{}, static_cast<S*>(out_dev), nullptr,
-                                                    ws, st),
-                       "mapreduce launch");
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "mapreduce") : rc;
-  });
-}
 
-int forge_dev_reduce_ordered(forge_op op, const void* src, uint64_t n, void* out_dev, void* ws,
-                             uint64_t ws_bytes, void* stream) {
-  forge::prim::detail::NvtxRange nvtx_range("forge_dev_reduce_ordered");
-  return guarded([&]() -> int {
-    int rc = menu::visit1(op, [&](auto e) -> int {
-      using E = decltype(e);
-      using T = typename E::T;
-      using S = typename E::S;
-      cudaStream_t st = static_cast<cudaStream_t>(stream);
-      if (n == 0)
-        return from_cuda(cudaMemcpyAsync(out_dev, &e.identity, sizeof(S), cudaMemcpyHostToDevice, st),
-                         "identity copy");
-      int w = require_ws(ws_bytes, cuda::OrderedReduceWs<S, typename E::Op>::bytes(cuda::mapreduce_max_grid()),
-                         "reduce_ordered");
-      if (w) return w;
-      return from_cuda(cuda::launch_reduce_ordered<T, S>(static_cast<const T*>(src), n, 1, typename E::F{},
-                                                         typename E::Op{}, static_cast<S*>(out_dev), nullptr,
-                                                         ws, st),
-                       "reduce_ordered launch");
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "reduce") : rc;
-  });
-}
 
-int forge_dev_scan(forge_op op, int32_t inclusive, const void* src, void* dst, uint64_t n,
-                   const void* carry_in_dev, void* total_out_dev, void* ws, uint64_t ws_bytes,
-                   void* stream) {
-  forge::prim::detail::NvtxRange nvtx_range("forge_dev_scan");
-  return guarded([&]() -> int {
-    int rc = menu::visit1(op, [&](auto e) -> int {
-      using E = decltype(e);
-      using T = typename E::T;
-      using S = typename E::S;
-      if (n == 0) return FORGE_OK;
-      int w = require_ws(ws_bytes, cuda::ScanWs<T, S, typename E::Op>::bytes(n), "scan");
-      if (w) return w;
-      return from_cuda(cuda::launch_scan<T, S>(static_cast<const T*>(src), 1, static_cast<S*>(dst), 1, n,
-                                               inclusive != 0, typename E::F{}, typename E::Op{}, e.identity,
-                                               static_cast<const S*>(carry_in_dev),
-                                               static_cast<S*>(total_out_dev), ws,
-                                               static_cast<cudaStream_t>(stream)),
-                       "scan launch");
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "scan") : rc;
-  });
-}
 
-int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* y,
-                     void* ws, uint64_t ws_bytes, void* stream) {
-  forge::prim::detail::NvtxRange nvtx_range("forge_dev_matvec");
-  return guarded([&]() -> int {
-    int rc = menu::visit2(op, [&](auto e) -> int {
-      using E = decltype(e);
-      using T = typename E::T;
-      using S = typename E::S;
-      int w = require_ws(ws_bytes, cuda::gevm_ws_bytes<T, S>(n, p_cols), "matvec");
-      if (w) return w;
-      auto st = static_cast<cudaStream_t>(stream);
-      cudaError_t err =
-          e.commutative
-              ? cuda::launch_gevm<T, S, typename E::F, typename E::Op, true, false>(
-                    static_cast<const T*>(A), n, p_cols, static_cast<const T*>(x), static_cast<S*>(y),
-                    typename E::F{}, typename E::Op{}, ws, st)
-              : cuda::launch_gevm<T, S, typename E::F, typename E::Op, true, true>(
-                    static_cast<const T*>(A), n, p_cols, static_cast<const T*>(x), static_cast<S*>(y),
-                    typename E::F{}, typename E::Op{}, ws, st);
-      return from_cuda(err, "matvec launch");
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "matrix") : rc;
-  });
-}
 
-int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* z,
-                     void* ws, uint64_t ws_bytes, void* stream) {
-  forge::prim::detail::NvtxRange nvtx_range("forge_dev_vecmat");
-  return guarded([&]() -> int {
-    int rc = menu::visit2(op, [&](auto e) -> int {
-      using E = decltype(e);
-      using T = typename E::T;
-      using S = typename E::S;
-      int w = require_ws(ws_bytes, cuda::gemv_ws_bytes<T, S>(n, p_cols), "vecmat");
-      if (w) return w;
-      return from_cuda(cuda::launch_gemv<T, S, typename E::F, typename E::Op, true>(
-                           static_cast<const T*>(A), n, p_cols, static_cast<const T*>(x), static_cast<S*>(z),
-                           typename E::F{}, typename E::Op{}, ws, static_cast<cudaStream_t>(stream)),
-                       "vecmat launch");
-    });
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "matrix") : rc;
-  });
-}
 
-int forge_dev_fold(forge_op op, const void* values_dev, uint32_t count, int32_t exclusive_upto,
-                   void* out_dev, int32_t* has_out_dev, void* stream) {
-  forge::prim::detail::NvtxRange nvtx_range("forge_dev_fold");
-  return guarded([&]() -> int {
-    auto go = [&](auto e) -> int {
-      using E = decltype(e);
-      using S = typename E::S;
-      return from_cuda(cuda::launch_fold<S>(static_cast<const S*>(values_dev), count, exclusive_upto,
-                                            typename E::Op{}, static_cast<S*>(out_dev), has_out_dev,
-                                            static_cast<cudaStream_t>(stream)),
-                       "fold launch");
-    };
-    int rc = menu::visit1(op, go);
-    if (rc == FORGE_ERR_UNSUPPORTED) rc = menu::visit2(op, go);
-    return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "fold") : rc;
-  });
-}
 
 int forge_dev_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
   forge::prim::detail::NvtxRange nvtx_range("forge_dev_copy");

@@ -11,9 +11,29 @@
 #include <cstdio>
 #include <mutex>
 
+#include <unordered_map>
+
+#include "forge/cuda/device.cuh"
 #include "forge/machine.hpp"
 
 namespace forge {
+
+namespace cuda {
+
+cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> last;  // workspace base -> layout tag
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = last.find(ws);
+    if (it != last.end() && it->second == tag) return cudaSuccess;
+    if (last.size() >= 4096) last.clear();  // forgetting only costs a memset on next use
+    last[ws] = tag;
+  }
+  return zero_bytes ? cudaMemsetAsync(ws, 0, zero_bytes, stream) : cudaSuccess;
+}
+
+}  // namespace cuda
 
 namespace {
 

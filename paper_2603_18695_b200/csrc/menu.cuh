@@ -71,11 +71,11 @@ struct AddF32 {
 struct AddF64 {
   FORGE_HD double operator()(double a, double b) const { return a + b; }
 };
-struct MaxF32 {
-  FORGE_HD float operator()(float a, float b) const { return a >= b ? a : b; }
+struct MaxF32 {  // NaN -> canonical NaN, -0 < +0: order-independent (algebra.hpp)
+  FORGE_HD float operator()(float a, float b) const { return fmax_total(a, b); }
 };
 struct MinF32 {
-  FORGE_HD float operator()(float a, float b) const { return a <= b ? a : b; }
+  FORGE_HD float operator()(float a, float b) const { return fmin_total(a, b); }
 };
 struct MaxI32 {
   FORGE_HD int32_t operator()(int32_t a, int32_t b) const { return a >= b ? a : b; }

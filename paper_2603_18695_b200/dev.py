@@ -51,21 +51,33 @@ def workspace_bytes(prim: int, op: int, n: int, p_cols: int = 0) -> int:
 
 class Workspace:
     """A zero-initialised device byte buffer, grown on demand.  The kernels
-    leave it reusable (self-resetting tickets / epochs); it must not be used by
-    two launches in flight at once."""
+    leave it reusable (self-resetting tickets / epochs) and the library
+    re-zeroes it when it moves to another primitive's layout, so one
+    Workspace may serve every primitive in turn; it must not be used by two
+    launches in flight at once."""
 
     def __init__(self, device=None):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.buf = torch.zeros(256, dtype=torch.uint8, device=self.device)
 
-    def ensure(self, nbytes: int) -> torch.Tensor:
+    def ensure(self, nbytes: int, stream=None) -> torch.Tensor:
+        """Grows the buffer to >= nbytes.  The new buffer is allocated and zeroed
+        ON `stream` (the stream the next kernel runs on), and the old one is
+        recorded on it so the caching allocator cannot hand its memory out
+        while kernels queued there may still use it."""
         if self.buf.numel() < nbytes:
-            self.buf = torch.zeros(max(nbytes, 2 * self.buf.numel()), dtype=torch.uint8, device=self.device)
+            s = torch.cuda.current_stream(self.device) if stream is None else stream
+            if not isinstance(s, torch.cuda.Stream):
+                s = torch.cuda.ExternalStream(int(s), device=self.device)
+            old = self.buf
+            with torch.cuda.stream(s):
+                self.buf = torch.zeros(max(nbytes, 2 * old.numel()), dtype=torch.uint8, device=self.device)
+            old.record_stream(s)
         return self.buf
 
-    def for_(self, prim: int, op: int, n: int, p_cols: int = 0) -> tuple[C.c_void_p, int]:
+    def for_(self, prim: int, op: int, n: int, p_cols: int = 0, stream=None) -> tuple[C.c_void_p, int]:
         need = workspace_bytes(prim, op, n, p_cols)
-        b = self.ensure(need)
+        b = self.ensure(need, stream)
         return C.c_void_p(b.data_ptr()), b.numel()
 
 
@@ -81,29 +93,29 @@ def fill_synthetic(op: int, dst: torch.Tensor, n: int, seed: int, index_base: in
 
 
 def mapreduce(op: int, src, n: int, out, ws: Workspace, stream=None) -> None:
-    w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n)
+    w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n, stream=stream)
     check(_lib().forge_dev_mapreduce(op, _ptr(src), n, _ptr(out), w, wb, _stream(stream)))
 
 
 def reduce_ordered(op: int, src, n: int, out, ws: Workspace, stream=None) -> None:
-    w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n)
+    w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n, stream=stream)
     check(_lib().forge_dev_reduce_ordered(op, _ptr(src), n, _ptr(out), w, wb, _stream(stream)))
 
 
 def scan(op: int, inclusive: bool, src, dst, n: int, ws: Workspace, carry_in=None, total_out=None,
          stream=None) -> None:
-    w, wb = ws.for_(capi.PRIM_SCAN, op, n)
+    w, wb = ws.for_(capi.PRIM_SCAN, op, n, stream=stream)
     check(_lib().forge_dev_scan(op, 1 if inclusive else 0, _ptr(src), _ptr(dst), n, _ptr(carry_in),
                                 _ptr(total_out), w, wb, _stream(stream)))
 
 
 def matvec(op: int, A, n: int, p_cols: int, x, y, ws: Workspace, stream=None) -> None:
-    w, wb = ws.for_(capi.PRIM_MATVEC, op, n, p_cols)
+    w, wb = ws.for_(capi.PRIM_MATVEC, op, n, p_cols, stream=stream)
     check(_lib().forge_dev_matvec(op, _ptr(A), n, p_cols, _ptr(x), _ptr(y), w, wb, _stream(stream)))
 
 
 def vecmat(op: int, A, n: int, p_cols: int, x, z, ws: Workspace, stream=None) -> None:
-    w, wb = ws.for_(capi.PRIM_VECMAT, op, n, p_cols)
+    w, wb = ws.for_(capi.PRIM_VECMAT, op, n, p_cols, stream=stream)
     check(_lib().forge_dev_vecmat(op, _ptr(A), n, p_cols, _ptr(x), _ptr(z), w, wb, _stream(stream)))
 
 

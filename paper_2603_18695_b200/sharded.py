@@ -33,7 +33,8 @@ class DeviceBackend:
     def __init__(self):
         from . import dev  # noqa: WPS433 (lazy: loads libforge.so)
         self.dev = dev
-        self.ws = dev.Workspace()
+        # one workspace per layout family: no re-zeroing when calls alternate
+        self.ws_reduce, self.ws_scan, self.ws_mat = dev.Workspace(), dev.Workspace(), dev.Workspace()
 
     def s_size(self, op: int) -> int:
         from .forge import op_info
@@ -47,22 +48,22 @@ class DeviceBackend:
         return torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
 
     def mapreduce(self, op, src, n, out):
-        self.dev.mapreduce(op, src, n, out, self.ws)
+        self.dev.mapreduce(op, src, n, out, self.ws_reduce)
 
     def reduce_ordered(self, op, src, n, out):
-        self.dev.reduce_ordered(op, src, n, out, self.ws)
+        self.dev.reduce_ordered(op, src, n, out, self.ws_reduce)
 
     def scan(self, op, inclusive, src, dst, n, carry_in):
-        self.dev.scan(op, inclusive, src, dst, n, self.ws, carry_in=carry_in)
+        self.dev.scan(op, inclusive, src, dst, n, self.ws_scan, carry_in=carry_in)
 
     def fold(self, op, values, count, out, exclusive_upto=-1):
         self.dev.fold(op, values, count, out, exclusive_upto=exclusive_upto)
 
     def matvec(self, op, A, n, p, x, y):
-        self.dev.matvec(op, A, n, p, x, y, self.ws)
+        self.dev.matvec(op, A, n, p, x, y, self.ws_mat)
 
     def vecmat(self, op, A, n, p, x, z):
-        self.dev.vecmat(op, A, n, p, x, z, self.ws)
+        self.dev.vecmat(op, A, n, p, x, z, self.ws_mat)
 
 
 @dataclass

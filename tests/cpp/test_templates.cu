@@ -340,6 +340,214 @@ void test_vcopy_struct(Machine& m) {
          "LaunchReport counters: one load and one store per element");
 }
 
+
+// ---- mixed-width map paths (algebra.hpp:15-28): u8 / u16 / i8
+// inputs promoted by the map to f32 / i32, through mapreduce and scan; plus a
+// 16-byte T scanned into a 4-byte S through make_scan_workspace<S> (a
+// workspace sized for S must fit every T: ADVICE r01).
+struct Half {  // u8 -> f32: x / 2 (exact)
+  FORGE_HD float operator()(uint8_t c) const { return 0.5f * float(c); }
+};
+struct Widen16 {  // u16 -> i32
+  FORGE_HD int32_t operator()(uint16_t c) const { return int32_t(c); }
+};
+struct SignedByte {  // i8 -> i32
+  FORGE_HD int32_t operator()(int8_t c) const { return int32_t(c); }
+};
+struct Quad {
+  uint32_t w[4];
+};
+struct QuadSum {  // 16-byte T -> 4-byte S (wrapping sum of the words)
+  FORGE_HD uint32_t operator()(const Quad& q) const { return q.w[0] + q.w[1] + q.w[2] + q.w[3]; }
+};
+}  // namespace
+namespace forge::intr {
+template <>
+struct TypeOf<Quad> {
+  static const TypeDescriptor& get() {
+    static const TypeDescriptor d = detail::tuple_of(Scalar::U32, 4);
+    return d;
+  }
+};
+}  // namespace forge::intr
+namespace {
+
+void test_mixed_width_maps(Machine& m) {
+  std::mt19937 rng(21);
+  ArchParams p;
+  for (uint64_t n : {1ull, 33ull, 4097ull, 1000003ull, 5000011ull}) {
+    std::vector<uint8_t> x8(n);
+    std::vector<uint16_t> x16(n);
+    std::vector<int8_t> xs8(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      x8[i] = uint8_t(rng());
+      x16[i] = uint16_t(rng());
+      xs8[i] = int8_t(rng());
+    }
+    BufferId b8 = upload(m, x8), b16 = upload(m, x16), bs8 = upload(m, xs8);
+    // u8 -> f32 sum: every partial sum is a multiple of 0.5 below 2^24, so exact
+    auto s_half = make_semiring<float>(Half{}, alg::Plus{}, std::optional<float>(0.f), true);
+    prim::Workspace wf = prim::make_mapreduce_workspace<float>(m, p);
+    float rf = 0;
+    LaunchReport r = prim::mapreduce(m, s_half, intr::make_view<uint8_t>(m, b8), wf, p, &rf);
+    double want = 0;
+    for (uint8_t c : x8) want += 0.5 * c;
+    EXPECT(r.ok && double(rf) == want, "u8->f32 mapreduce n=%llu: %g vs %g", (unsigned long long)n, rf, want);
+    // u16 -> i32 wrapping sum, u16 max
+    auto s_w = make_semiring<int32_t>(Widen16{}, alg::WrapPlusI32{}, std::optional<int32_t>(0), true);
+    prim::Workspace wi = prim::make_mapreduce_workspace<int32_t>(m, p);
+    int32_t ri = 0;
+    r = prim::mapreduce(m, s_w, intr::make_view<uint16_t>(m, b16), wi, p, &ri);
+    uint32_t wsum = 0;
+    for (uint16_t c : x16) wsum += c;
+    EXPECT(r.ok && uint32_t(ri) == wsum, "u16->i32 mapreduce n=%llu", (unsigned long long)n);
+    // i8 -> i32 inclusive scan (exact), and u8 -> f32 exclusive scan
+    auto s_sb = make_semiring<int32_t>(SignedByte{}, alg::WrapPlusI32{}, std::optional<int32_t>(0), true);
+    BufferId d32 = intr::create_buffer<int32_t>(m, n), df = intr::create_buffer<float>(m, n);
+    prim::Workspace ws = prim::make_scan_workspace<int32_t>(m, n, p);
+    r = prim::scan(m, s_sb, intr::make_view<int8_t>(m, bs8), intr::make_view<int32_t>(m, d32), true, ws, p);
+    auto g32 = download<int32_t>(m, d32, n);
+    bool ok = r.ok;
+    int32_t acc = 0;
+    for (uint64_t i = 0; i < n && ok; ++i) ok = g32[i] == (acc += xs8[i]);
+    EXPECT(ok, "i8->i32 scan n=%llu", (unsigned long long)n);
+    prim::Workspace wsf = prim::make_scan_workspace<float>(m, n, p);
+    r = prim::scan(m, s_half, intr::make_view<uint8_t>(m, b8), intr::make_view<float>(m, df), false, wsf, p);
+    auto gf = download<float>(m, df, n);
+    ok = r.ok;
+    double accf = 0;
+    for (uint64_t i = 0; i < n && ok; ++i) {
+      ok = double(gf[i]) == accf;
+      accf += 0.5 * x8[i];
+    }
+    EXPECT(ok, "u8->f32 exclusive scan n=%llu", (unsigned long long)n);
+    // 16-byte T -> 4-byte S scan with the S-sized workspace
+    std::vector<Quad> q(n);
+    for (auto& v : q)
+      for (auto& w : v.w) w = rng();
+    BufferId bq = upload(m, q);
+    auto s_q = make_semiring<uint32_t>(QuadSum{}, alg::Plus{}, std::optional<uint32_t>(0u), true);
+    prim::Workspace wq = prim::make_scan_workspace<uint32_t>(m, n, p);
+    BufferId du = intr::create_buffer<uint32_t>(m, n);
+    r = prim::scan(m, s_q, intr::make_view<Quad>(m, bq), intr::make_view<uint32_t>(m, du), true, wq, p);
+    auto gu = download<uint32_t>(m, du, n);
+    ok = r.ok;
+    uint32_t accu = 0;
+    for (uint64_t i = 0; i < n && ok; ++i) ok = gu[i] == (accu += QuadSum{}(q[i]));
+    EXPECT(ok, "16-byte T -> 4-byte S scan through make_scan_workspace<S> n=%llu", (unsigned long long)n);
+    for (BufferId b : {b8, b16, bs8, d32, df, bq, du}) m.destroy_buffer(b);
+    for (prim::Workspace* w : {&wf, &wi, &ws, &wsf, &wq}) w->release(m);
+  }
+}
+
+// ---- one workspace buffer serving several primitives and matrix shapes in
+// turn (layouts overlap; the library re-zeroes on a layout change)
+void test_workspace_shared_across_primitives(Machine& m) {
+  ArchParams p;
+  std::mt19937 rng(33);
+  const uint64_t nt = 200003, pt = 8;   // tall-skinny: gevm splits rows (tickets + partials)
+  const uint64_t nw = 1000, pw = 60000; // short-wide: gemv splits columns
+  std::vector<int32_t> At(nt * pt), xt(nt), Aw(nw * pw), xw(pw), v(nt);
+  for (auto& e : At) e = int32_t(rng() % 1000);
+  for (auto& e : xt) e = int32_t(rng() % 1000);
+  for (auto& e : Aw) e = int32_t(rng() % 1000);
+  for (auto& e : xw) e = int32_t(rng() % 1000);
+  for (auto& e : v) e = int32_t(rng());
+  auto pt_spec = make_semiring<int32_t>(alg::WrapTimesI32{}, alg::WrapPlusI32{}, std::optional<int32_t>(0), true);
+  auto sum = make_semiring<int32_t>(alg::Identity{}, alg::WrapPlusI32{}, std::optional<int32_t>(0), true);
+  BufferId bAt = upload(m, At), bxt = upload(m, xt), bAw = upload(m, Aw), bxw = upload(m, xw), bv = upload(m, v);
+  BufferId y = intr::create_buffer<int32_t>(m, pt), z = intr::create_buffer<int32_t>(m, nw);
+  BufferId sd = intr::create_buffer<int32_t>(m, nt);
+  // one byte buffer big enough for every layout, wired into every field
+  const uint64_t big = std::max({prim::required_workspace(prim::Primitive::MatVec, 4, nt, pt, p),
+                                 prim::required_workspace(prim::Primitive::VecMat, 4, nw, pw, p),
+                                 prim::required_workspace(prim::Primitive::Scan, 4, nt, 0, p),
+                                 prim::required_workspace(prim::Primitive::MapReduce, 4, nt, 0, p)});
+  prim::Workspace ws;
+  ws.partials = ws.tile_flag = intr::create_buffer<uint8_t>(m, big, 256);
+  ws.result = intr::create_buffer<uint8_t>(m, 64, 256);
+  std::vector<uint32_t> wy(pt, 0), wz(nw, 0);
+  for (uint64_t j = 0; j < pt; ++j)
+    for (uint64_t i = 0; i < nt; ++i) wy[j] += uint32_t(xt[i]) * uint32_t(At[j * nt + i]);
+  for (uint64_t i = 0; i < nw; ++i)
+    for (uint64_t j = 0; j < pw; ++j) wz[i] += uint32_t(Aw[j * nw + i]) * uint32_t(xw[j]);
+  uint32_t wsum = 0;
+  for (int32_t e : v) wsum += uint32_t(e);
+  bool ok = true;
+  for (int round = 0; round < 3; ++round) {
+    prim::matvec<int32_t, int32_t>(m, pt_spec, intr::make_view<int32_t>(m, bAt), nt, pt, intr::make_view<int32_t>(m, bxt),
+                                   intr::make_view<int32_t>(m, y), ws, p);
+    auto gy = download<int32_t>(m, y, pt);
+    for (uint64_t j = 0; j < pt; ++j) ok = ok && uint32_t(gy[j]) == wy[j];
+    prim::scan(m, sum, intr::make_view<int32_t>(m, bv), intr::make_view<int32_t>(m, sd), true, ws, p);
+    auto gs = download<int32_t>(m, sd, nt);
+    uint32_t acc = 0;
+    for (uint64_t i = 0; i < nt; ++i) ok = ok && uint32_t(gs[i]) == (acc += uint32_t(v[i]));
+    prim::vecmat<int32_t, int32_t>(m, pt_spec, intr::make_view<int32_t>(m, bAw), nw, pw, intr::make_view<int32_t>(m, bxw),
+                                   intr::make_view<int32_t>(m, z), ws, p);
+    auto gz = download<int32_t>(m, z, nw);
+    for (uint64_t i = 0; i < nw; ++i) ok = ok && uint32_t(gz[i]) == wz[i];
+    int32_t r = 0;
+    prim::mapreduce(m, sum, intr::make_view<int32_t>(m, bv), ws, p, &r);
+    ok = ok && uint32_t(r) == wsum;
+  }
+  EXPECT(ok, "one workspace buffer shared by matvec / scan / vecmat / mapreduce, 3 rounds");
+  for (BufferId b : {bAt, bxt, bAw, bxw, bv, y, z, sd, ws.partials, ws.result}) m.destroy_buffer(b);
+}
+
+// ---- reference API re-exports: MatPlan / tall_slices / plan_mat
+// (primitives.hpp:202-244) with the reference's own numbers,
+// TypeOf<OptVal<S>> (:840-853), sat_add_i32 (algebra.hpp:85-90)
+void test_reference_api_reexports(Machine& m) {
+  ArchParams p;
+  prim::MatPlan w = prim::plan_mat(16384, 16384, true, p);
+  EXPECT(w.wide && w.cfg.num_blocks == 200 && w.cfg.threads_per_block == 128,
+         "plan_mat C4 commutative: wide 200x128 (got wide=%d %ux%u)", int(w.wide), w.cfg.num_blocks,
+         w.cfg.threads_per_block);
+  prim::MatPlan t = prim::plan_mat(16384, 16384, false, p);
+  EXPECT(!t.wide && t.nb == 2 && t.cfg.num_blocks == 400 && t.cfg.threads_per_block == 256 && t.slots == 2 * 16384,
+         "plan_mat C4 non-commutative: tall nb=2 400x256");
+  EXPECT(prim::tall_slices(1, p) == 1 && prim::tall_slices(8192, p) == 1 && prim::tall_slices(8193, p) == 2 &&
+             prim::tall_slices(uint64_t(1) << 40, p) == 100,
+         "tall_slices clamps to [1, mapreduce_blocks]");
+  prim::MatPlan b = prim::b200_plan_mat<float>(prim::Primitive::MatVec, 16384, 16384, true);
+  prim::MatPlan bv = prim::b200_plan_mat<float>(prim::Primitive::VecMat, 16384, 16384, true);
+  EXPECT(b.wide && b.cfg.num_blocks > 0 && bv.nb >= 1 && bv.cfg.num_blocks > 0, "b200_plan_mat geometry");
+  EXPECT(intr::descriptor_of<prim::OptVal<float>>() == parse_descriptor("struct(f32@0,u8@4;size=8)"),
+         "TypeOf<OptVal<f32>> = %s", to_string(intr::descriptor_of<prim::OptVal<float>>()).c_str());
+  EXPECT(intr::descriptor_of<prim::OptVal<alg::Mat2>>() ==
+             parse_descriptor("struct(tuple(u32,u32,u32,u32)@0,u8@16;size=20)"),
+         "TypeOf<OptVal<Mat2>> = %s", to_string(intr::descriptor_of<prim::OptVal<alg::Mat2>>()).c_str());
+  // sat_add_i32 saturates, so it is NOT associative near the limits: the
+  // reference's validate_reduce_op must reject it there and accept it on
+  // small values (where it is plain addition)
+  std::mt19937 rng(4);
+  auto eqi = [](int32_t a, int32_t b) { return a == b; };
+  auto sat = [](int32_t a, int32_t b) { return alg::sat_add_i32(a, b); };
+  const bool big = prim::validate_reduce_op<int32_t>(sat, std::optional<int32_t>(0), true,
+                                                     [&] { return int32_t(rng()); }, eqi);
+  const bool small = prim::validate_reduce_op<int32_t>(sat, std::optional<int32_t>(0), true,
+                                                       [&] { return int32_t(rng() % 1000) - 500; }, eqi);
+  EXPECT(!big && small, "sat_add_i32: validate_reduce_op rejects saturation, accepts small values");
+  EXPECT(alg::sat_add_i32(INT32_MAX, 1) == INT32_MAX && alg::sat_add_i32(INT32_MIN, -1) == INT32_MIN &&
+             alg::sat_add_i32(2, 3) == 5,
+         "sat_add_i32 known answers");
+  // ... and on the device, as a mapreduce over values that never saturate
+  std::vector<int32_t> x(100003);
+  int64_t want = 0;
+  for (auto& e : x) want += (e = int32_t(rng() % 20001) - 10000);
+  BufferId bx = upload(m, x);
+  auto spec = make_semiring<int32_t>(alg::Identity{}, [] __host__ __device__(int32_t a, int32_t c) {
+    return alg::sat_add_i32(a, c);
+  }, std::optional<int32_t>(0), true);
+  prim::Workspace wm = prim::make_mapreduce_workspace<int32_t>(m, p);
+  int32_t r = 0;
+  LaunchReport rep = prim::mapreduce(m, spec, intr::make_view<int32_t>(m, bx), wm, p, &r);
+  EXPECT(rep.ok && int64_t(r) == want, "sat_add_i32 mapreduce on the device");
+  wm.release(m);
+  m.destroy_buffer(bx);
+}
+
 }  // namespace
 
 int main() {
@@ -356,6 +564,9 @@ int main() {
   test_noncommutative_matvec(m);
   test_errors_and_params(m);
   test_vcopy_struct(m);
+  test_mixed_width_maps(m);
+  test_workspace_shared_across_primitives(m);
+  test_reference_api_reexports(m);
   std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "PASS", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

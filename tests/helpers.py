@@ -9,7 +9,8 @@ from oracle import oracle as orc
 # Parity tolerances: |got - exact_64| <= tol * sum|terms|.
 TOL = {0: 1e-5, 1: 1e-5, 4: 1e-12, 10: 1e-5, 13: 1e-5, 14: 1e-5, 15: 1e-5, 32: 1e-5, 36: 1e-12}
 
-SIZES = [1, 31, 32, 33, 255, 256, 257, 4095, 4096, 4097, 100_000, 1_000_000]
+# SPEC.md:512's sweep plus BASELINE C1 (2^20: whole 8192-element tiles, no tail)
+SIZES = [0, 1, 31, 32, 33, 255, 256, 257, 4095, 4096, 4097, 100_000, 1_000_000, 1 << 20]
 OPS_1D = list(range(16))
 COMMUTATIVE_1D = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 14, 15]
 OPS_2D = [32, 33, 34, 35, 36, 37]

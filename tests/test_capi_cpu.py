@@ -74,10 +74,23 @@ def test_descriptor_literals():
 def test_arch_params_defaults_and_workspace_sizing():
     p = F.ArchParams()
     assert (p.warp_width, p.mapreduce_blocks, p.threads_per_block, p.nitem_scan) == (32, 100, 256, 16)
-    # B200 workspace sizes: scan tile = 4096 f32 -> 1 tile state (16 B with the f64 carry) + control
+    # B200 workspace sizes: 256-byte control block + one 256-byte state slot per
+    # 8192-f32 tile of the smem kernel (full speed); never less than the general
+    # kernel's 4096-element tiles at packed 16-byte states (the f64 carry)
     assert F.required_workspace(capi.PRIM_SCAN, 4, 4096) == 256 + 256
-    assert F.required_workspace(capi.PRIM_SCAN, 4, 4097) == 256 + 512
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 8192) == 256 + 256
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 8193) == 256 + 512
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 1 << 33) == 256 + (1 << 20) * 256
     assert F.required_workspace(capi.PRIM_VCOPY, 4, 100) == 0
+    # the reference-facing bound covers the device layer's need for every menu op
+    # (a workspace made for S fits every T: ADVICE r01)
+    lib = capi.load()
+    for op in capi.OPS_1D:
+        ss = F.op_info(op)["s_size"]
+        for n in (1, 4095, 4097, 100_003, 1 << 24):
+            need = C.c_uint64()
+            assert lib.forge_dev_workspace_bytes(capi.PRIM_SCAN, op, n, 0, C.byref(need)) == 0
+            assert F.required_workspace(capi.PRIM_SCAN, ss, n) >= need.value, (op, n)
     with pytest.raises(F.ForgeError) as e:
         F.required_workspace(capi.PRIM_SCAN, 4, 10, params=F.ArchParams(warp_width=64, threads_per_block=256))
     assert e.value.name == "Unsupported"

@@ -20,9 +20,23 @@ def test_cpp_templates_user_types():
     assert r.stdout.strip().splitlines()[-1].startswith("PASS")
 
 
+@pytest.mark.gpu
+def test_cpp_composite_shuffle_spec7():
+    # SPEC.md acceptance #7: 100 random descriptors (MisalignedStruct included)
+    # x 128 random values x every source lane / delta, through the sm_100a
+    # word-wise shuffles (tests/cpp/test_shuffle.cu)
+    b = BIN.parent / "test_shuffle"
+    assert b.exists(), "tests/cpp/test_shuffle not built (run __graft_entry__.build())"
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().splitlines()[-1].startswith("PASS")
+
+
 def test_cpp_templates_source_present():
     # CPU-side: the test program exists and exercises every template primitive.
     src = (BIN.parent / "test_templates.cu").read_text()
     for name in ("prim::scan", "prim::mapreduce", "prim::matvec", "prim::vecmat", "prim::mapreduce_2d",
-                 "prim::vcopy", "validate_reduce_op"):
+                 "prim::vcopy", "validate_reduce_op", "prim::plan_mat", "prim::tall_slices", "sat_add_i32",
+                 "OptVal"):
         assert name in src

@@ -23,10 +23,14 @@ def m():
 
 
 def upload(m, op, arr, which="T", pad=0):
-    buf = F.create_buffer(m, op, len(arr) + pad, which=which)
+    buf = F.create_buffer(m, op, max(len(arr) + pad, 1), which=which)
     if len(arr):
         m.write(buf, arr)
     return buf
+
+
+def view_n(buf, n):
+    return F.View(buf, 0, n, 1)
 
 
 # ---------------------------------------------------------------------------
@@ -38,7 +42,7 @@ def test_mapreduce_matches_oracle(m, op, n):
     x = orc.fill(op, n, seed_for(op, n), variant=1 if op == 15 else 0)
     buf = upload(m, op, x)
     ws = F.make_mapreduce_workspace(m, op)
-    got, rep = F.mapreduce(m, F.make_semiring(op), F.make_view(m, buf), ws)
+    got, rep = F.mapreduce(m, F.make_semiring(op), view_n(buf, n), ws)
     assert rep.ok
     want, ex, sc = orc.mapreduce(op, x)
     assert_match(op, np.array([got], dtype=F.s_dtype(op)), np.array([want]), ex, sc, f"mapreduce n={n}")
@@ -106,11 +110,11 @@ def test_scan_matches_oracle(m, op, n, inclusive):
         pytest.skip("quaternion products: 10^4..10^5 covers SPEC.md:515")
     x = orc.fill(op, n, seed_for(op, n, inclusive), variant=1 if op == 15 else 0)
     a = upload(m, op, x)
-    d = F.create_buffer(m, op, n, which="S")
+    d = F.create_buffer(m, op, max(n, 1), which="S")
     ws = F.make_scan_workspace(m, op, n)
-    rep = F.scan(m, F.make_semiring(op), F.make_view(m, a), F.make_view(m, d), inclusive, ws)
+    rep = F.scan(m, F.make_semiring(op), view_n(a, n), view_n(d, n), inclusive, ws)
     assert rep.ok
-    got = m.read(d, n, F.s_dtype(op))
+    got = m.read(d, n, F.s_dtype(op)) if n else np.zeros(0, F.s_dtype(op))
     want, ex, sc = orc.scan(op, inclusive, x)
     assert_match(op, got, want, ex, sc, f"scan n={n} incl={inclusive}")
     F.release(m, ws)

@@ -66,6 +66,47 @@ def test_mapreduce_relaunch_stress():
     assert np.all(got == want)
 
 
+@pytest.mark.parametrize("op", [capi.I32_SUM, capi.MAT2_U32])
+def test_relaxed_protocol_mutant_is_caught(op):
+    # The ordering ablation (MutationFlags::relax_scan_flag,
+    # reference primitives.hpp:64-67): with the epoch tag of the tile states
+    # ignored, a tile may accept a predecessor's state left by the PREVIOUS
+    # launch on the same workspace.  The relaunch stress — two different inputs
+    # alternating on one workspace, every output checked bit for bit — must
+    # catch that mutant, and must pass the product protocol.
+    lib = capi.load()
+    n = 64 * 8192 + 17
+    xs = []
+    for k in range(2):
+        x = dev.empty(op, n)
+        dev.fill_synthetic(op, x, n, 0xAB1A + k)
+        xs.append(x)
+    want = []
+    ws = dev.Workspace()
+    for k in range(2):
+        y = dev.empty(op, n, "S")
+        dev.scan(op, True, xs[k], y, n, ws)
+        got = y.cpu().numpy().view(np.uint8).view(F.s_dtype(op))
+        assert orc.check_scan_synthetic(op, True, n, 0xAB1A + k, got, 0)[0] == 0
+        want.append(y)
+
+    def mismatches(relax: bool, launches: int = 60) -> int:
+        assert lib.forge_set_mutation_flags(1 if relax else 0, 0) == 0
+        try:
+            bad = 0
+            y = dev.empty(op, n, "S")
+            for i in range(launches):
+                dev.scan(op, True, xs[i % 2], y, n, ws)
+                bad += int(not torch.equal(y, want[i % 2]))
+            return bad
+        finally:
+            lib.forge_set_mutation_flags(0, 0)
+
+    assert mismatches(relax=False) == 0, "product protocol must pass the stress"
+    assert mismatches(relax=True) > 0, "the relaxed-protocol mutant escaped the stress test"
+    assert mismatches(relax=False) == 0
+
+
 @pytest.mark.skipif(shutil.which("compute-sanitizer") is None, reason="compute-sanitizer not on PATH")
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer_clean(tool):

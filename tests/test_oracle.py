@@ -214,3 +214,21 @@ def test_check_scan_synthetic_at_matches_full_check(op, inclusive):
     raw[k:k + 4] ^= np.frombuffer(np.float32(1.5).tobytes(), np.uint8)
     bad, _ = orc.check_scan_synthetic_at(op, inclusive, seed, idx, raw.view(got_at.dtype), 1e-5)
     assert bad == 1
+
+
+@pytest.mark.parametrize("op", [2, 3, 11])  # f32 max, f32 min, arg-max
+def test_oracle_special_values_order_independent(op):
+    # The order-independent max / min / arg-max (NaN canonical or first-NaN,
+    # -0 < +0): any permutation of special-value data folds to the same bits,
+    # which is what lets a GPU tree match the sequential oracle bit for bit.
+    x = orc.fill(op, 20_000, 0xC0FFEE + op, variant=2)
+    r0 = np.atleast_1d(orc.mapreduce(op, x)[0]).view(np.uint8).tobytes()
+    rng = np.random.default_rng(op)
+    for _ in range(5):
+        y = x[rng.permutation(len(x))]
+        assert np.atleast_1d(orc.mapreduce(op, y)[0]).view(np.uint8).tobytes() == r0
+    # and a reassociated fold (pairwise halves) agrees too
+    h = len(x) // 2
+    a, b = orc.mapreduce(op, x[:h])[0], orc.mapreduce(op, x[h:])[0]
+    pair = np.concatenate([np.atleast_1d(a), np.atleast_1d(b)]).astype(x.dtype)
+    assert np.atleast_1d(orc.mapreduce(op, pair)[0]).view(np.uint8).tobytes() == r0
