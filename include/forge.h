@@ -287,6 +287,15 @@ int forge_vcopy(forge_machine* m, forge_view src, forge_view dst, uint32_t nitem
  * product protocol. */
 int forge_set_mutation_flags(int32_t relax_scan_flag, int32_t relax_mapreduce_flag);
 
+/* Adversarial schedule for the calling thread's subsequent scans, the B200
+ * counterpart of the reference simulator's seeded schedules (ScheduleSeed,
+ * machine.hpp:122-128).  TEST ONLY: seed != 0 makes a pseudo-random 1/8 of the
+ * tiles (chosen by the seed) wait delay_ns before publishing their aggregate,
+ * so their successors poll unpublished states.  Results are unchanged (the
+ * protocol waits); without it B200 CTAs publish in ticket order and the
+ * ablation above is never exercised.  seed = 0 turns it off. */
+int forge_set_schedule_perturbation(uint64_t seed, uint32_t delay_ns);
+
 /* vload_pattern (intrinsics.hpp:190, intrinsics.cpp:29-33). segs has room for 16. */
 int forge_vload_pattern(uint64_t offset, uint32_t nitem, uint32_t* segs, uint32_t* count);
 
@@ -324,6 +333,14 @@ int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, co
                      void* y, void* ws, uint64_t ws_bytes, void* stream);
 int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x,
                      void* z, void* ws, uint64_t ws_bytes, void* stream);
+/* The same over an n x p block of a larger column-major matrix whose columns
+ * are `lda` >= n elements apart (0 = n): A points at the block's first element.
+ * A row block [lo, hi) of a global n_g x p matrix G is (G + lo, hi - lo, p,
+ * lda = n_g) — the vecmat shard of SURVEY.md §8(e), consumed in place. */
+int forge_dev_matvec_lda(forge_op op, const void* A, uint64_t n, uint64_t p_cols, uint64_t lda,
+                         const void* x, void* y, void* ws, uint64_t ws_bytes, void* stream);
+int forge_dev_vecmat_lda(forge_op op, const void* A, uint64_t n, uint64_t p_cols, uint64_t lda,
+                         const void* x, void* z, void* ws, uint64_t ws_bytes, void* stream);
 
 /* Fold of values[0..count-1] in index order (the rank-order fold of the sharded
  * exchange).  exclusive_upto >= 0 folds only values[0..exclusive_upto-1] and

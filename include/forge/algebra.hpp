@@ -14,6 +14,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <limits>
 
 #include "forge/intrinsics.hpp"
@@ -124,27 +125,54 @@ FORGE_HD AffineT<F> affine_compose(const AffineT<F>& p, const AffineT<F>& q) {
 // ---- order-independent f32 max / min.  The reference's
 // `a >= b ? a : b` is neither commutative on ±0 nor associative with NaN, so
 // a GPU tree and a sequential fold could disagree bit-wise on such inputs.
-// Here: any NaN operand gives the canonical quiet NaN (0x7fc00000); -0 < +0
-// (max(-0, +0) = +0, min(-0, +0) = -0).  On ordinary values it equals the
-// reference operator exactly.
-FORGE_HD float canonical_nan_f32() { return std::numeric_limits<float>::quiet_NaN(); }
+// Here: any NaN operand gives the canonical NaN 0x7fffffff (the PTX canonical
+// NaN, so the device needs no fix-up); -0 < +0 (max(-0, +0) = +0,
+// min(-0, +0) = -0).  On ordinary values it equals the reference operator.
+// Device: one FMNMX.NAN instruction (max.NaN / min.NaN).
 FORGE_HD bool is_nan_f32(float x) { return x != x; }
-FORGE_HD bool sign_bit_f32(float x) {
+FORGE_HD uint32_t f32_bits(float x) {
 #if defined(__CUDA_ARCH__)
-  return __float_as_uint(x) >> 31;
+  return __float_as_uint(x);
 #else
-  return std::signbit(x);
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return u;
 #endif
 }
+FORGE_HD float f32_from_bits(uint32_t u) {
+#if defined(__CUDA_ARCH__)
+  return __uint_as_float(u);
+#else
+  float x;
+  std::memcpy(&x, &u, 4);
+  return x;
+#endif
+}
+inline constexpr uint32_t kCanonicalNaN32 = 0x7fffffffu;
+
 FORGE_HD float fmax_total(float a, float b) {
-  if (is_nan_f32(a) || is_nan_f32(b)) return canonical_nan_f32();
-  if (a == b) return sign_bit_f32(a) ? b : a;  // equal: differ at most in the sign of zero
+#if defined(__CUDA_ARCH__)
+  // FMNMX.NAN: NaN -> 0x7fffffff, and -0 < +0 in either operand order
+  // (measured on B200, tools/probe_minmax.cu) — exactly the semantics above
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+#else
+  if (is_nan_f32(a) || is_nan_f32(b)) return f32_from_bits(kCanonicalNaN32);
+  if (a == b) return std::signbit(a) ? b : a;  // equal: differ at most in the sign of zero
   return a > b ? a : b;
+#endif
 }
 FORGE_HD float fmin_total(float a, float b) {
-  if (is_nan_f32(a) || is_nan_f32(b)) return canonical_nan_f32();
-  if (a == b) return sign_bit_f32(a) ? a : b;
+#if defined(__CUDA_ARCH__)
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+#else
+  if (is_nan_f32(a) || is_nan_f32(b)) return f32_from_bits(kCanonicalNaN32);
+  if (a == b) return std::signbit(a) ? a : b;
   return a < b ? a : b;
+#endif
 }
 
 struct ArgMax {
@@ -155,15 +183,12 @@ struct ArgMax {
 // max by v, ties to the smaller i.  NaN values rank above every number (the
 // arg-max of data containing NaN is its first NaN); -0 == +0 ties by index.
 // A total preorder on v, so the op is associative and commutative for every
-// input, NaN included.
+// input, NaN included.  (Branch-free selects: as cheap as the NaN-unaware form.)
 FORGE_HD ArgMax argmax_combine(const ArgMax& a, const ArgMax& b) {
   const bool an = is_nan_f32(a.v), bn = is_nan_f32(b.v);
-  if (an != bn) return an ? a : b;
-  if (!an) {
-    if (a.v > b.v) return a;
-    if (b.v > a.v) return b;
-  }
-  return a.i <= b.i ? a : b;
+  const bool ta = (a.v > b.v) | (an & !bn);
+  const bool tb = (b.v > a.v) | (bn & !an);
+  return (ta | (!tb & (a.i <= b.i))) ? a : b;
 }
 
 // ---- operator helpers (algebra.hpp:85-100)

@@ -40,6 +40,7 @@ struct GevmArgs {
   const T* x;  // nullable when !UsesX
   S* y;
   uint64_t n, p;
+  uint64_t lda;  // elements between columns (>= n): a block of a larger column-major matrix
   F2 f;        // f(x_elem, a_elem)
   Op op;
   uint32_t ks;              // row splits per column
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(kMatThreads) gevm_kernel(const GevmArgs<T, S, 
   const uint32_t s = uint32_t(item % a.ks);
   const uint64_t r0 = uint64_t(s) * a.rows_per_split;
   const uint64_t r1 = r0 + a.rows_per_split < a.n ? r0 + a.rows_per_split : a.n;
-  const T* col = a.A + j * a.n;
+  const T* col = a.A + j * a.lda;
   const T xz{};
   auto fx = [&](const T& xv, const T& av) { return a.f(UsesX ? xv : xz, av); };
 
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kMatThreads, MINB) gevm_cols_kernel(const Gevm
     if constexpr (UsesX) load_items<T, VE, false>(a.x + i, xx);
 #pragma unroll
     for (int c = 0; c < CPW; ++c)
-      if (c < nc) load_items<T, VE>(a.A + (j0 + c) * a.n + i, av[c]);
+      if (c < nc) load_items<T, VE>(a.A + (j0 + c) * a.lda + i, av[c]);
 #pragma unroll
     for (int c = 0; c < CPW; ++c) {
 #pragma unroll
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kMatThreads, MINB) gevm_cols_kernel(const Gevm
   for (uint64_t i = r0 + nv * VE + lane; i < r1; i += kWarp) {
 #pragma unroll
     for (int c = 0; c < CPW; ++c)
-      if (c < nc) part[c] = opt_combine(a.op, part[c], Opt<S>{fx(UsesX ? a.x[i] : xz, a.A[(j0 + c) * a.n + i]), true});
+      if (c < nc) part[c] = opt_combine(a.op, part[c], Opt<S>{fx(UsesX ? a.x[i] : xz, a.A[(j0 + c) * a.lda + i]), true});
   }
 #pragma unroll
   for (int c = 0; c < CPW; ++c) part[c] = warp_allreduce_comm(a.op, part[c]);
@@ -244,6 +245,7 @@ struct GemvArgs {
   const T* x;
   S* z;
   uint64_t n, p;
+  uint64_t lda;  // elements between columns (>= n): a row block of a larger matrix, in place
   F2 f;  // f(a_elem, x_elem)
   Op op;
   uint32_t ks;              // column splits
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, 
       uint64_t j = c0;
       {
         T av[VE];
-        load_items<T, VE>(a.A + j * a.n + i0, av);
+        load_items<T, VE>(a.A + j * a.lda + i0, av);
         const T xj = UsesX ? a.x[j] : xz;
 #pragma unroll
         for (int e = 0; e < VE; ++e) acc[e] = fa(av[e], xj);
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, 
         T xj[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          load_items<T, VE>(a.A + (j + u) * a.n + i0, av[u]);
+          load_items<T, VE>(a.A + (j + u) * a.lda + i0, av[u]);
           xj[u] = UsesX ? a.x[j + u] : xz;
         }
 #pragma unroll
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, 
       }
       for (; j < c1; ++j) {
         T av[VE];
-        load_items<T, VE>(a.A + j * a.n + i0, av);
+        load_items<T, VE>(a.A + j * a.lda + i0, av);
         const T xj = UsesX ? a.x[j] : xz;
 #pragma unroll
         for (int e = 0; e < VE; ++e) acc[e] = a.op(acc[e], fa(av[e], xj));
@@ -313,8 +315,8 @@ __global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, 
       for (int e = 0; e < VE; ++e) {
         const uint64_t i = i0 + e;
         if (i < a.n) {
-          S v = fa(a.A[c0 * a.n + i], UsesX ? a.x[c0] : xz);
-          for (uint64_t j = c0 + 1; j < c1; ++j) v = a.op(v, fa(a.A[j * a.n + i], UsesX ? a.x[j] : xz));
+          S v = fa(a.A[c0 * a.lda + i], UsesX ? a.x[c0] : xz);
+          for (uint64_t j = c0 + 1; j < c1; ++j) v = a.op(v, fa(a.A[j * a.lda + i], UsesX ? a.x[j] : xz));
           acc[e] = v;
         }
       }
@@ -531,15 +533,21 @@ inline uint64_t gemv_ws_bytes(uint64_t n, uint64_t p) {
          round_up(uint64_t(pl.ks) * n * sizeof(S), 256) + (pl.groups > 1 ? uint64_t(pl.groups) * n * sizeof(S) : 0);
 }
 
+// `lda` (>= n, 0 = n): elements between consecutive columns of A, so a block of
+// a larger column-major matrix (rows [lo, lo+n) of p of its columns: A + lo +
+// j0 * lda) is consumed in place — the row-block shard of vecmat and the
+// sub-matrix of a sharded matvec.
 template <class T, class S, class F2, class Op, bool UsesX, bool Ordered>
 cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, const F2& f,
-                        const Op& op, void* ws, cudaStream_t stream) {
+                        const Op& op, void* ws, cudaStream_t stream, uint64_t lda = 0) {
   if (p == 0 || n == 0) return cudaSuccess;
+  if (lda == 0) lda = n;
+  if (lda < n) return cudaErrorInvalidValue;
   constexpr int VE = mr_vec_elems<T>();
-  const bool vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && (!UsesX || is_aligned(x, 32));
+  const bool vec = VE > 1 && is_aligned(A, 32) && (lda * sizeof(T)) % 32 == 0 && (!UsesX || is_aligned(x, 32));
   const bool cols = !Ordered && vec && gevm_cols_enabled();
   GevmPlan pl = cols ? plan_gevm_cols<T>(n, p) : plan_gevm<T>(n, p);
-  GevmArgs<T, S, F2, Op> a{A, x, y, n, p, f, op, pl.ks, pl.rows_per_split, vec, nullptr, nullptr};
+  GevmArgs<T, S, F2, Op> a{A, x, y, n, p, lda, f, op, pl.ks, pl.rows_per_split, vec, nullptr, nullptr};
   if (pl.ks > 1) {
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);
@@ -560,13 +568,15 @@ cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, co
 
 template <class T, class S, class F2, class Op, bool UsesX>
 cudaError_t launch_gemv(const T* A, uint64_t n, uint64_t p, const T* x, S* z, const F2& f,
-                        const Op& op, void* ws, cudaStream_t stream) {
+                        const Op& op, void* ws, cudaStream_t stream, uint64_t lda = 0) {
   if (p == 0 || n == 0) return cudaSuccess;
+  if (lda == 0) lda = n;
+  if (lda < n) return cudaErrorInvalidValue;
   constexpr int VE = gemv_vec_elems<T>();
   GemvPlan pl = plan_gemv<T>(n, p);
-  GemvArgs<T, S, F2, Op> a{A,     x,     z,     n,     p,       f,       op, pl.ks, pl.cols_per_split, pl.row_blocks,
+  GemvArgs<T, S, F2, Op> a{A,  x,     z,     n,     p,       lda,     f, op, pl.ks, pl.cols_per_split, pl.row_blocks,
                            false, nullptr, nullptr, pl.gsize, pl.groups, nullptr};
-  a.vec = VE > 1 && is_aligned(A, 32) && (n * sizeof(T)) % 32 == 0 && is_aligned(z, 32);
+  a.vec = VE > 1 && is_aligned(A, 32) && (lda * sizeof(T)) % 32 == 0 && is_aligned(z, 32);
   if (pl.ks > 1) {
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);

@@ -132,6 +132,26 @@ struct ScanArgs {
   uint32_t backoff_ns;    // look-back: sleep between polls of INVALID states (0; FORGE_DEV knob)
   uint32_t epoch_mask;    // 0x3fffffff; 0 = the relax_scan_flag ablation (MutationFlags,
                           // primitives.hpp:64-67): stale states of earlier launches are accepted
+  uint64_t perturb_seed;  // test schedule perturbation (ScanTestHooks), 0 = off
+  uint32_t perturb_ns;
+};
+
+// Test-only hooks of one scan launch (both off in production):
+//   relax_epoch   the relax_scan_flag ablation (MutationFlags, reference
+//                 primitives.hpp:64-67): the epoch tag of tile states is
+//                 ignored, so a state left by an earlier launch on the same
+//                 workspace is accepted as if it were published by this one;
+//   perturb_seed  the B200 counterpart of the simulator's adversarial
+//   perturb_ns    schedules (ScheduleSeed, machine.hpp): a pseudo-random 1/8 of
+//                 the tiles (chosen by the seed) wait perturb_ns before
+//                 publishing their aggregate, so successors poll states that
+//                 are not yet published.  Measured on B200: without it no tile
+//                 ever polls an unpublished predecessor (CTAs launch, load and
+//                 publish in ticket order), and the ablation goes unseen.
+struct ScanTestHooks {
+  bool relax_epoch = false;
+  uint64_t perturb_seed = 0;
+  uint32_t perturb_ns = 0;
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -297,7 +317,13 @@ __device__ __forceinline__ void block_exclusive_prefix(
     }
   } else {
     const C agg_c = M::to_c(agg.v);
-    if (threadIdx.x == 0) IO::write(a.states, tile, a.state_stride, epoch, kPartial, agg_c);
+    if (threadIdx.x == 0) {
+      if (a.perturb_ns && ((tile * 0x9E3779B97F4A7C15ull) ^ a.perturb_seed) % 8 == 0) {  // test hook
+        const uint64_t t0 = global_ns();
+        while (global_ns() - t0 < a.perturb_ns) __nanosleep(200);
+      }
+      IO::write(a.states, tile, a.state_stride, epoch, kPartial, agg_c);
+    }
     Opt<C> carry{C{}, false};  // meaningful in thread 0
     if (a.lookback == kLookbackSkipProbe) {
       // development ceiling probe (FORGE_SCAN_LOOKBACK=99): no look-back, WRONG results
@@ -729,14 +755,12 @@ inline uint64_t* scan_trace_for(uint64_t tiles) {
 // kernel that runs; ScanWs::bytes(n) gives full-speed slots), zeroed once at
 // creation.  Returns cudaErrorInvalidValue when the workspace is too small
 // (callers check first and raise WorkspaceTooSmall).
-// `relax_epoch` is the relax_scan_flag ablation (MutationFlags): states of
-// earlier launches on the same workspace are accepted — a deliberately broken
-// protocol that the relaunch stress tests must catch (tests/test_gpu_stress.py).
+// `hooks`: test-only ablation / schedule perturbation (ScanTestHooks).
 template <class T, class S, class F, class Op>
 cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_stride, uint64_t n,
                         bool inclusive, const F& f, const Op& op, const S& identity,
                         const S* carry_in, S* total_out, void* ws, uint64_t ws_bytes, cudaStream_t stream,
-                        bool relax_epoch = false) {
+                        const ScanTestHooks& hooks = {}) {
   using WsT = ScanWs<T, S, Op>;
   if (n == 0) return cudaSuccess;
   if (ceil_div(n, WsT::kTileGeneral) >= (1ull << 31)) return cudaErrorInvalidValue;
@@ -744,7 +768,8 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                           f,        op,       identity,  carry_in,   total_out,
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
                           static_cast<uint32_t*>(ws), 0u, 0u, scan_lookback_mode(), nullptr,
-                          scan_backoff_ns(), relax_epoch ? 0u : 0x3fffffffu};
+                          scan_backoff_ns(), hooks.relax_epoch ? 0u : 0x3fffffffu, hooks.perturb_seed,
+                          hooks.perturb_ns};
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.

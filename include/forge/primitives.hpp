@@ -21,8 +21,10 @@
 //     error.hpp:18, never raised there).
 //   * The geometry fields of ArchParams are validated like the reference but
 //     the kernels choose their own tiles / grids; RunOptions::backend,
-//     schedule and tuning are accepted and ignored (there is no simulator and
-//     no CPU fallback).  mutate.relax_scan_flag selects the scan ablation (tile
+//     tuning are accepted and ignored (there is no simulator and no CPU
+//     fallback); a non-zero schedule.seed perturbs the scan's schedule the B200
+//     way (1/8 of the tiles, chosen by the seed, publish 20 us late:
+//     cuda::ScanTestHooks) — results are unchanged, only slower.  mutate.relax_scan_flag selects the scan ablation (tile
 //     states of earlier launches accepted: a broken publication protocol the
 //     stress tests must catch); relax_mapreduce_flag is accepted and ignored
 //     (the mapreduce never waits on another block's flag).
@@ -554,7 +556,8 @@ LaunchReport scan(Machine& m, const SemiringSpec<F, S, Op>& spec, View<T> src, V
     k = 1;
     return cuda::launch_scan<T, S, F, Op>(sp, src.stride, dp, dst.stride, n, inclusive, spec.map, spec.op, ident,
                                           nullptr, nullptr, wsp, ws_bytes, m.stream(),
-                                          opt.mutate.relax_scan_flag);
+                                          cuda::ScanTestHooks{opt.mutate.relax_scan_flag, opt.schedule.seed,
+                                                              opt.schedule.seed ? 20000u : 0u});
   });
   detail::count_load(rep, src.buf, n);
   detail::count_store(rep, dst.buf, n);

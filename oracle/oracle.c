@@ -238,11 +238,11 @@ static forge_mat2_u32 mat2_mul(forge_mat2_u32 a, forge_mat2_u32 b) { /* algebra.
 }
 
 /* Order-independent f32 max / min (include/forge/algebra.hpp fmax_total):
- * NaN -> canonical quiet NaN, -0 < +0.  Equal to the reference's
+ * NaN -> the canonical NaN 0x7fffffff (PTX's), -0 < +0.  Equal to the reference's
  * `a >= b ? a : b` (algebra ops of SPEC.md) on NaN-free inputs without
  * zero-sign ties, where that operator is itself order-dependent. */
 static float canonical_nan(void) {
-  const uint32_t bits = 0x7fc00000u;
+  const uint32_t bits = 0x7fffffffu;
   float f;
   memcpy(&f, &bits, 4);
   return f;

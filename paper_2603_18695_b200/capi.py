@@ -132,6 +132,7 @@ _SIGNATURES = {
                                      C.POINTER(ArchParams), C.POINTER(LaunchReport)]),
     "forge_vcopy": (C.c_int, [_P, View, View, _u32, C.POINTER(ArchParams), C.POINTER(LaunchReport)]),
     "forge_set_mutation_flags": (C.c_int, [_i32, _i32]),
+    "forge_set_schedule_perturbation": (C.c_int, [_u64, _u32]),
     "forge_vload_pattern": (C.c_int, [_u64, _u32, C.POINTER(_u32), C.POINTER(_u32)]),
     "forge_dev_workspace_bytes": (C.c_int, [C.c_int, C.c_int, _u64, _u64, C.POINTER(_u64)]),
     "forge_dev_mapreduce": (C.c_int, [C.c_int, _P, _u64, _P, _P, _u64, _P]),
@@ -139,6 +140,8 @@ _SIGNATURES = {
     "forge_dev_scan": (C.c_int, [C.c_int, _i32, _P, _P, _u64, _P, _P, _P, _u64, _P]),
     "forge_dev_matvec": (C.c_int, [C.c_int, _P, _u64, _u64, _P, _P, _P, _u64, _P]),
     "forge_dev_vecmat": (C.c_int, [C.c_int, _P, _u64, _u64, _P, _P, _P, _u64, _P]),
+    "forge_dev_matvec_lda": (C.c_int, [C.c_int, _P, _u64, _u64, _u64, _P, _P, _P, _u64, _P]),
+    "forge_dev_vecmat_lda": (C.c_int, [C.c_int, _P, _u64, _u64, _u64, _P, _P, _P, _u64, _P]),
     "forge_dev_fold": (C.c_int, [C.c_int, _P, _u32, _i32, _P, _P, _P]),
     "forge_dev_copy": (C.c_int, [_P, _P, _u64, _P]),
     "forge_dev_fill_synthetic": (C.c_int, [C.c_int, _P, _u64, _u64, _u64, _i32, _P]),

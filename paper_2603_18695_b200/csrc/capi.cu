@@ -330,6 +330,12 @@ int forge_set_mutation_flags(int32_t relax_scan_flag, int32_t relax_mapreduce_fl
   return FORGE_OK;
 }
 
+int forge_set_schedule_perturbation(uint64_t seed, uint32_t delay_ns) {
+  g_perturb_seed = seed;
+  g_perturb_ns = seed ? delay_ns : 0;
+  return FORGE_OK;
+}
+
 
 
 

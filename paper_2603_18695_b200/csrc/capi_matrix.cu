@@ -35,10 +35,11 @@ int forge_vecmat(forge_machine* m, forge_semiring spec, forge_view A, uint64_t n
   });
 }
 
-int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* y,
-                     void* ws, uint64_t ws_bytes, void* stream) {
+int forge_dev_matvec_lda(forge_op op, const void* A, uint64_t n, uint64_t p_cols, uint64_t lda, const void* x,
+                         void* y, void* ws, uint64_t ws_bytes, void* stream) {
   forge::prim::detail::NvtxRange nvtx_range("forge_dev_matvec");
   return guarded([&]() -> int {
+    if (lda != 0 && lda < n) raise(ErrorCode::InvalidArgument, "matvec: lda < n");
     int rc = menu::visit2(op, [&](auto e) -> int {
       using E = decltype(e);
       using T = typename E::T;
@@ -50,20 +51,26 @@ int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, co
           e.commutative
               ? cuda::launch_gevm<T, S, typename E::F, typename E::Op, true, false>(
                     static_cast<const T*>(A), n, p_cols, static_cast<const T*>(x), static_cast<S*>(y),
-                    typename E::F{}, typename E::Op{}, ws, st)
+                    typename E::F{}, typename E::Op{}, ws, st, lda)
               : cuda::launch_gevm<T, S, typename E::F, typename E::Op, true, true>(
                     static_cast<const T*>(A), n, p_cols, static_cast<const T*>(x), static_cast<S*>(y),
-                    typename E::F{}, typename E::Op{}, ws, st);
+                    typename E::F{}, typename E::Op{}, ws, st, lda);
       return from_cuda(err, "matvec launch");
     });
     return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "matrix") : rc;
   });
 }
 
-int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* z,
+int forge_dev_matvec(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* y,
                      void* ws, uint64_t ws_bytes, void* stream) {
+  return forge_dev_matvec_lda(op, A, n, p_cols, n, x, y, ws, ws_bytes, stream);
+}
+
+int forge_dev_vecmat_lda(forge_op op, const void* A, uint64_t n, uint64_t p_cols, uint64_t lda, const void* x,
+                         void* z, void* ws, uint64_t ws_bytes, void* stream) {
   forge::prim::detail::NvtxRange nvtx_range("forge_dev_vecmat");
   return guarded([&]() -> int {
+    if (lda != 0 && lda < n) raise(ErrorCode::InvalidArgument, "vecmat: lda < n");
     int rc = menu::visit2(op, [&](auto e) -> int {
       using E = decltype(e);
       using T = typename E::T;
@@ -72,11 +79,16 @@ int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, co
       if (w) return w;
       return from_cuda(cuda::launch_gemv<T, S, typename E::F, typename E::Op, true>(
                            static_cast<const T*>(A), n, p_cols, static_cast<const T*>(x), static_cast<S*>(z),
-                           typename E::F{}, typename E::Op{}, ws, static_cast<cudaStream_t>(stream)),
+                           typename E::F{}, typename E::Op{}, ws, static_cast<cudaStream_t>(stream), lda),
                        "vecmat launch");
     });
     return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "matrix") : rc;
   });
+}
+
+int forge_dev_vecmat(forge_op op, const void* A, uint64_t n, uint64_t p_cols, const void* x, void* z,
+                     void* ws, uint64_t ws_bytes, void* stream) {
+  return forge_dev_vecmat_lda(op, A, n, p_cols, n, x, z, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

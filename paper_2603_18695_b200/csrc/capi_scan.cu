@@ -12,6 +12,7 @@ int forge_scan(forge_machine* m, forge_semiring spec, forge_view src, forge_view
       using E = decltype(e);
       prim::RunOptions ro;
       ro.mutate = g_mutate;
+      ro.schedule.seed = g_perturb_seed;
       LaunchReport r = prim::scan(m->m, e.spec(spec.has_identity != 0), view_of<typename E::T>(src),
                                   view_of<typename E::S>(dst), inclusive != 0, w, to_params(params), ro);
       return finish(r, report);
@@ -37,7 +38,7 @@ int forge_dev_scan(forge_op op, int32_t inclusive, const void* src, void* dst, u
                                                inclusive != 0, typename E::F{}, typename E::Op{}, e.identity,
                                                static_cast<const S*>(carry_in_dev),
                                                static_cast<S*>(total_out_dev), ws, ws_bytes,
-                                               static_cast<cudaStream_t>(stream), g_mutate.relax_scan_flag),
+                                               static_cast<cudaStream_t>(stream), scan_hooks()),
                        "scan launch");
     });
     return rc == FORGE_ERR_UNSUPPORTED ? unsupported_op(op, "scan") : rc;

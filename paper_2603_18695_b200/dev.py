@@ -109,14 +109,17 @@ def scan(op: int, inclusive: bool, src, dst, n: int, ws: Workspace, carry_in=Non
                                 _ptr(total_out), w, wb, _stream(stream)))
 
 
-def matvec(op: int, A, n: int, p_cols: int, x, y, ws: Workspace, stream=None) -> None:
+def matvec(op: int, A, n: int, p_cols: int, x, y, ws: Workspace, stream=None, lda: int = 0) -> None:
+    """y[j] = op_i f(x[i], A[i,j]) over an n x p column-major A whose columns are
+    `lda` (0 = n) elements apart; A may be a pointer (int) into a larger matrix."""
     w, wb = ws.for_(capi.PRIM_MATVEC, op, n, p_cols, stream=stream)
-    check(_lib().forge_dev_matvec(op, _ptr(A), n, p_cols, _ptr(x), _ptr(y), w, wb, _stream(stream)))
+    check(_lib().forge_dev_matvec_lda(op, _ptr(A), n, p_cols, lda, _ptr(x), _ptr(y), w, wb, _stream(stream)))
 
 
-def vecmat(op: int, A, n: int, p_cols: int, x, z, ws: Workspace, stream=None) -> None:
+def vecmat(op: int, A, n: int, p_cols: int, x, z, ws: Workspace, stream=None, lda: int = 0) -> None:
+    """z[i] = op_j f(A[i,j], x[j]); see matvec for `lda`."""
     w, wb = ws.for_(capi.PRIM_VECMAT, op, n, p_cols, stream=stream)
-    check(_lib().forge_dev_vecmat(op, _ptr(A), n, p_cols, _ptr(x), _ptr(z), w, wb, _stream(stream)))
+    check(_lib().forge_dev_vecmat_lda(op, _ptr(A), n, p_cols, lda, _ptr(x), _ptr(z), w, wb, _stream(stream)))
 
 
 def fold(op: int, values, count: int, out, exclusive_upto: int = -1, has_out=None, stream=None) -> None:

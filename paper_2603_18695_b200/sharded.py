@@ -10,9 +10,17 @@
              totals[0..rank) into a device carry -> local single-pass scan seeded
              with that carry (no host synchronisation anywhere).  HBM traffic
              3n/G per GPU.
-  matvec     (gevm, y = x^T A) columns sharded: independent, no collective.
-  vecmat     (gemv, z = A x)  rows sharded: each rank holds its (n/G) x p block;
-             independent, no collective.
+  matvec     (gevm, y = x^T A, reference primitives.hpp:776-791) columns
+             sharded in contiguous blocks: rank r folds columns
+             shard_of(p, r, G) of the column-major A — its own n x p_r block
+             (contiguous), or the block IN PLACE in a replicated global A
+             (pointer + lo*n, lda = n).  No collective; optional all-gather of
+             the y blocks into the full y on every rank.
+  vecmat     (gemv, z = A x, primitives.hpp:795-807) rows sharded: rank r
+             folds rows shard_of(n, r, G) — its own n_r x p block (lda = n_r),
+             or the rows in place in a replicated global A (pointer + lo,
+             lda = n; forge_dev_vecmat_lda).  No collective; optional
+             all-gather of the z blocks.
 
 The collective is torch.distributed (NCCL over NVLink/NVSwitch on B200s; gloo in
 the CPU tests).  The local compute is a backend object: `DeviceBackend` calls
@@ -59,11 +67,16 @@ class DeviceBackend:
     def fold(self, op, values, count, out, exclusive_upto=-1):
         self.dev.fold(op, values, count, out, exclusive_upto=exclusive_upto)
 
-    def matvec(self, op, A, n, p, x, y):
-        self.dev.matvec(op, A, n, p, x, y, self.ws_mat)
+    def _at(self, op, A, a_offset):
+        if a_offset == 0:
+            return A
+        return A.data_ptr() + a_offset * self.t_size(op)
 
-    def vecmat(self, op, A, n, p, x, z):
-        self.dev.vecmat(op, A, n, p, x, z, self.ws_mat)
+    def matvec(self, op, A, n, p, x, y, lda=0, a_offset=0):
+        self.dev.matvec(op, self._at(op, A, a_offset), n, p, x, y, self.ws_mat, lda=lda)
+
+    def vecmat(self, op, A, n, p, x, z, lda=0, a_offset=0):
+        self.dev.vecmat(op, self._at(op, A, a_offset), n, p, x, z, self.ws_mat, lda=lda)
 
 
 @dataclass
@@ -140,15 +153,55 @@ def sharded_scan(op: int, inclusive: bool, local_src, local_dst, n_local: int, b
     return totals
 
 
-def sharded_matvec(op: int, A_local, n: int, p_local: int, x, y_local, backend=None):
-    """gevm over a column block: rank r owns columns [lo, hi) of the n x p
-    column-major A (contiguous in memory) and produces y[lo:hi]."""
-    be = backend or DeviceBackend()
-    be.matvec(op, A_local, n, p_local, x, y_local)
+def _all_gather_blocks(local: torch.Tensor, total: int, elem_size: int, world: int, out: torch.Tensor,
+                       group=None) -> None:
+    """All-gather of contiguous output blocks (block r = shard_of(total, r, world),
+    ragged) into `out` (total * elem_size bytes) on every rank, in rank order."""
+    width = ((total + world - 1) // world) * elem_size
+    pad = torch.zeros(width, dtype=torch.uint8, device=local.device)
+    nb = local.numel()
+    if nb:
+        pad[:nb].copy_(local.reshape(-1)[:nb])
+    g = _all_gather_bytes(pad, world, group).view(world, width)
+    for r in range(world):
+        sh = shard_of(total, r, world)
+        if sh.n:
+            out[sh.lo * elem_size: sh.hi * elem_size].copy_(g[r, : sh.n * elem_size])
 
 
-def sharded_vecmat(op: int, A_local, n_local: int, p: int, x, z_local, backend=None):
-    """gemv over a row block: rank r owns the (n_local x p) column-major block of
-    rows [lo, hi) and produces z[lo:hi]."""
+def sharded_matvec(op: int, A, n: int, p: int, x, y_local, *, in_place: bool = False, gather_into=None,
+                   backend=None, group=None) -> Shard:
+    """gevm y = x^T A over the GLOBAL n x p column-major A, columns sharded:
+    this rank computes y[lo:hi] for its columns [lo, hi) = shard_of(p, rank, G).
+    `A` is this rank's n x (hi-lo) column block, or (in_place=True) the whole
+    replicated A whose block is read in place.  `x` is the full length-n vector.
+    `gather_into` (optional, p outputs): every rank receives the full y."""
     be = backend or DeviceBackend()
-    be.vecmat(op, A_local, n_local, p, x, z_local)
+    rank, world = _world(group)
+    sh = shard_of(p, rank, world)
+    if sh.n:
+        be.matvec(op, A, n, sh.n, x, y_local, lda=n, a_offset=sh.lo * n if in_place else 0)
+    if gather_into is not None:
+        _all_gather_blocks(y_local, p, be.s_size(op), world, gather_into, group)
+    return sh
+
+
+def sharded_vecmat(op: int, A, n: int, p: int, x, z_local, *, in_place: bool = False, gather_into=None,
+                   backend=None, group=None) -> Shard:
+    """gemv z = A x over the GLOBAL n x p column-major A, rows sharded: this rank
+    computes z[lo:hi] for its rows [lo, hi) = shard_of(n, rank, G).  `A` is
+    this rank's (hi-lo) x p block (column-major, lda = hi-lo), or
+    (in_place=True) the whole replicated A whose rows are read in place
+    (lda = n: a row block of a column-major matrix is strided).  `x` is the full
+    length-p vector; `gather_into` (optional, n outputs) all-gathers z."""
+    be = backend or DeviceBackend()
+    rank, world = _world(group)
+    sh = shard_of(n, rank, world)
+    if sh.n:
+        if in_place:
+            be.vecmat(op, A, sh.n, p, x, z_local, lda=n, a_offset=sh.lo)
+        else:
+            be.vecmat(op, A, sh.n, p, x, z_local, lda=sh.n)
+    if gather_into is not None:
+        _all_gather_blocks(z_local, n, be.s_size(op), world, gather_into, group)
+    return sh

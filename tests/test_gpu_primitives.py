@@ -151,9 +151,15 @@ def test_scan_errors(m):
     with pytest.raises(F.ForgeError) as e:
         F.scan(m, F.make_semiring(F.I32_SUM, identity=False), F.make_view(m, a), F.make_view(m, d4), False, ws)
     assert e.value.name == "MissingIdentity"
+    # a workspace made for 4 elements holds 32 packed tile states: a 100_000-
+    # element scan fits (at packed slots), a 10^7-element one does not
     small = F.make_scan_workspace(m, F.I32_SUM, 4)
-    big = upload(m, F.I32_SUM, np.zeros(100_000, np.int32))
-    bd = F.create_buffer(m, F.I32_SUM, 100_000, which="S")
+    mid = upload(m, F.I32_SUM, np.arange(100_000, dtype=np.int32))
+    md = F.create_buffer(m, F.I32_SUM, 100_000, which="S")
+    assert F.scan(m, F.make_semiring(F.I32_SUM), F.make_view(m, mid), F.make_view(m, md), True, small).ok
+    assert np.array_equal(m.read(md, 100_000, np.int32), np.cumsum(np.arange(100_000), dtype=np.int64).astype(np.int32))
+    big = upload(m, F.I32_SUM, np.zeros(10_000_000, np.int32))
+    bd = F.create_buffer(m, F.I32_SUM, 10_000_000, which="S")
     with pytest.raises(F.ForgeError) as e:
         F.scan(m, F.make_semiring(F.I32_SUM), F.make_view(m, big), F.make_view(m, bd), True, small)
     assert e.value.name == "WorkspaceTooSmall"

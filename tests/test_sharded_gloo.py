@@ -55,6 +55,22 @@ class OracleBackend:
             v, _, _ = orc.mapreduce(fop, np.ascontiguousarray(vals))
             self._put(out, np.array([v], dtype=orc.s_dtype(op)).tobytes())
 
+    def _block(self, op, A, n, p, lda, a_offset):
+        lda = lda or n
+        flat = self._arr(A, orc.t_dtype(op), A.numel() // orc.t_dtype(op).itemsize)
+        cols = [flat[a_offset + j * lda: a_offset + j * lda + n] for j in range(p)]
+        return np.ascontiguousarray(np.concatenate(cols)) if p else flat[:0]
+
+    def matvec(self, op, A, n, p, x, y, lda=0, a_offset=0):
+        blk = self._block(op, A, n, p, lda, a_offset)
+        v, _, _ = orc.matvec(op, blk, n, p, self._arr(x, orc.t_dtype(op), n))
+        self._put(y, v.tobytes())
+
+    def vecmat(self, op, A, n, p, x, z, lda=0, a_offset=0):
+        blk = self._block(op, A, n, p, lda, a_offset)
+        v, _, _ = orc.vecmat(op, blk, n, p, self._arr(x, orc.t_dtype(op), p))
+        self._put(z, v.tobytes())
+
     def scan(self, op, inclusive, src, dst, n, carry_in):
         carry = None if carry_in is None else self._arr(carry_in, orc.s_dtype(op), 1)[0]
         y, _, _ = orc.scan(op, inclusive, self._arr(src, orc.t_dtype(op), n), carry=carry)
@@ -74,9 +90,31 @@ def _worker(rank, world, port, cases, q):
     be = OracleBackend()
     results = []
     for kind, op, n, inclusive, seed in cases:
-        x = orc.fill(op, n, seed)
-        sh = sharded.shard_of(n, rank, world)
-        src = torch.from_numpy(x[sh.lo:sh.hi].view(np.uint8).copy())
+        if kind not in ("matvec", "vecmat"):
+            x = orc.fill(op, n, seed)
+            sh = sharded.shard_of(n, rank, world)
+            src = torch.from_numpy(x[sh.lo:sh.hi].view(np.uint8).copy())
+        if kind in ("matvec", "vecmat"):
+            (nn, pp), in_place = n, inclusive
+            A = orc.fill(op, nn * pp, seed)
+            xv = orc.fill(op, nn if kind == "matvec" else pp, seed + 1)
+            ss = orc.s_dtype(op).itemsize
+            total = pp if kind == "matvec" else nn
+            sh = sharded.shard_of(total, rank, world)
+            if in_place:
+                At = torch.from_numpy(A.view(np.uint8).copy())
+            elif kind == "matvec":  # the rank's own column block (contiguous)
+                At = torch.from_numpy(A[sh.lo * nn: sh.hi * nn].view(np.uint8).copy())
+            else:  # the rank's own row block, column-major with lda = rows
+                blk = A.reshape(pp, nn)[:, sh.lo:sh.hi]
+                At = torch.from_numpy(np.ascontiguousarray(blk).reshape(-1).view(np.uint8).copy())
+            loc = torch.zeros(max(sh.n, 1) * ss, dtype=torch.uint8)
+            full = torch.zeros(total * ss, dtype=torch.uint8)
+            fn = sharded.sharded_matvec if kind == "matvec" else sharded.sharded_vecmat
+            fn(op, At, nn, pp, torch.from_numpy(xv.view(np.uint8).copy()), loc, in_place=in_place,
+               gather_into=full, backend=be)
+            results.append((loc.numpy().tobytes()[: sh.n * ss], full.numpy().tobytes()))
+            continue
         if kind == "mapreduce":
             r = sharded.sharded_mapreduce(op, src, sh.n, backend=be)
             results.append(r.numpy().tobytes()[: orc.s_dtype(op).itemsize])
@@ -102,6 +140,16 @@ CASES = [
     ("scan", 0, 20_000, True, 10),
     ("scan", 10, 2048, False, 11),
     ("scan", 5, 2, True, 12),      # fewer elements than ranks for world 3
+    # matrix shards: (kind, op, (n, p), in_place, seed); column / row blocks,
+    # own blocks and in place in a replicated A (lda), ragged and tiny shapes
+    ("matvec", 33, (517, 301), False, 13),   # min-plus: exact
+    ("matvec", 35, (300, 7), True, 14),      # i32 plus-times: exact
+    ("matvec", 37, (64, 5), False, 15),      # Mat2: ordered, non-commutative
+    ("matvec", 32, (1000, 130), True, 16),   # f32
+    ("vecmat", 33, (701, 90), False, 17),
+    ("vecmat", 35, (257, 33), True, 18),
+    ("vecmat", 37, (50, 9), True, 19),
+    ("vecmat", 32, (2, 400), False, 20),     # fewer rows than ranks for world 3
 ]
 
 
@@ -118,6 +166,19 @@ def test_sharded_exchange_gloo(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     for ci, (kind, op, n, inclusive, seed) in enumerate(CASES):
+        if kind in ("matvec", "vecmat"):
+            nn, pp = n
+            A = orc.fill(op, nn * pp, seed)
+            xv = orc.fill(op, nn if kind == "matvec" else pp, seed + 1)
+            want, ex, sc = (orc.matvec if kind == "matvec" else orc.vecmat)(op, A, nn, pp, xv)
+            blocks = np.frombuffer(b"".join(got[r][ci][0] for r in range(world)), dtype=orc.s_dtype(op))
+            for g in [blocks] + [np.frombuffer(got[r][ci][1], dtype=orc.s_dtype(op)) for r in range(world)]:
+                assert len(g) == len(want)
+                if orc.ncomp(op):
+                    assert orc.within(op, g, ex, sc, 1e-5)[0], (kind, op)
+                else:
+                    assert g.tobytes() == want.tobytes(), (kind, op, n)
+            continue
         x = orc.fill(op, n, seed)
         if kind == "mapreduce":
             want, ex, sc = orc.mapreduce(op, x)

@@ -1,3 +1,5 @@
-# Scratch GPU experiment (development; overwritten per experiment)
 mkdir -p gpurun_out
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_step.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-breakdown --no-sharded-scan > gpurun_out/bench_ncu.log 2>&1
+timeout 300 python tools/debug_mutant.py > gpurun_out/mutant.log 2>&1
+timeout 300 python tools/probe.py scan > gpurun_out/probe.log 2>&1
+timeout 300 python tools/probe.py matrix >> gpurun_out/probe.log 2>&1
+timeout 1800 python -m pytest tests/test_gpu_semantics.py -q --timeout 600 -p no:randomly > gpurun_out/pytest.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/pytest.log
