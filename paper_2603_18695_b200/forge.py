@@ -219,6 +219,10 @@ class Machine:
                                       out.nbytes))
         return out
 
+    def read_ptr(self, buf: int, host_ptr: int, nbytes: int, elem_offset: int = 0) -> None:
+        """forge_read_bytes into caller host memory (e.g. a pinned buffer)."""
+        check(_lib().forge_read_bytes(self.handle, buf, elem_offset, C.c_void_p(host_ptr), nbytes))
+
     def fill_zero(self, buf: int) -> None:
         check(_lib().forge_fill_zero(self.handle, buf))
 

@@ -53,7 +53,8 @@ class DeviceBackend:
         return op_info(op)["t_size"]
 
     def new_bytes(self, nbytes: int) -> torch.Tensor:
-        return torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        # every byte is written by a kernel before it is read: no fill kernel
+        return torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 
     def mapreduce(self, op, src, n, out):
         self.dev.mapreduce(op, src, n, out, self.ws_reduce)
@@ -122,6 +123,10 @@ def sharded_mapreduce(op: int, local_src, n_local: int, backend=None, group=None
     be = backend or DeviceBackend()
     rank, world = _world(group)
     ss = be.s_size(op)
+    if world == 1:  # one shard: the local mapreduce is the result
+        result = be.new_bytes(ss)
+        be.mapreduce(op, local_src, n_local, result)
+        return result
     part = be.new_bytes(ss)
     be.mapreduce(op, local_src, n_local, part)
     gathered = _all_gather_bytes(part, world, group)

@@ -1,40 +1,34 @@
-"""Development: does the scan look-back ever read a predecessor's state before
-the predecessor publishes it in the current launch?  (a) relax_scan_flag
-mutant, alternating inputs; (b) product build with the epoch rewound so the
-previous launch's states carry the current epoch."""
+"""Development: relaxed-protocol mutant vs schedule perturbation, per op:
+number of mismatching elements per launch (alternating inputs, one workspace)."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 from paper_2603_18695_b200 import capi, dev
 lib = capi.load()
-op = capi.I32_SUM
 out = {}
-for n in (1 << 20, 1 << 24, 1 << 26):
+for op in (capi.I32_SUM, capi.F32_SUM, capi.MAT2_U32):
+    n = (1 << 22) + 17
     xs = []
     for k in range(2):
-        x = dev.empty(op, n); dev.fill_synthetic(op, x, n, 100 + k); xs.append(x)
+        x = dev.empty(op, n); dev.fill_synthetic(op, x, n, 0xAB1A ^ (k * 0x5A5A << 40)); xs.append(x)
     ws = dev.Workspace()
     want = []
     for k in range(2):
         y = dev.empty(op, n, "S"); dev.scan(op, True, xs[k], y, n, ws); want.append(y)
     y = dev.empty(op, n, "S")
     res = {}
-    for relax in (0, 1):
+    for relax, seed, ns in ((0, 0, 0), (1, 0, 0), (0, 0x5EED, 20000), (1, 0x5EED, 20000), (1, 0x5EED, 100000)):
         lib.forge_set_mutation_flags(relax, 0)
+        lib.forge_set_schedule_perturbation(seed, ns)
         bad = []
-        for i in range(10):
+        for i in range(6):
+            y.fill_(0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             dev.scan(op, True, xs[i % 2], y, n, ws)
-            bad.append(int((y.view(torch.int32) != want[i % 2].view(torch.int32)).sum().item()))
-        lib.forge_set_mutation_flags(0, 0)
-        res[f"relax{relax}"] = bad
-    # rewind the epoch: ctrl word 2 of the workspace
-    bad = []
-    for i in range(10):
-        e = ws.buf[8:12].clone()
-        dev.scan(op, True, xs[i % 2], y, n, ws)
-        torch.cuda.synchronize()
-        ws.buf[8:12].copy_(e)  # next launch reuses this launch's epoch
-        bad.append(int((y.view(torch.int32) != want[i % 2].view(torch.int32)).sum().item()))
-    res["rewound"] = bad
-    out[n] = res
-print(json.dumps(out))
+            e1.record(); torch.cuda.synchronize()
+            bad.append((int((y != want[i % 2]).sum().item()), round(e0.elapsed_time(e1), 3)))
+        lib.forge_set_mutation_flags(0, 0); lib.forge_set_schedule_perturbation(0, 0)
+        res[f"relax{relax}_seed{seed}_{ns}"] = bad
+    out[op] = res
+print(json.dumps(out, indent=1))

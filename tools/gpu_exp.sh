@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
 timeout 300 python tools/debug_mutant.py > gpurun_out/mutant.log 2>&1
-timeout 300 python tools/probe.py scan > gpurun_out/probe.log 2>&1
-timeout 300 python tools/probe.py matrix >> gpurun_out/probe.log 2>&1
-timeout 1800 python -m pytest tests/test_gpu_semantics.py -q --timeout 600 -p no:randomly > gpurun_out/pytest.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/pytest.log
+timeout 900 python bench.py --steps 5 > gpurun_out/bench.log 2>&1; echo "bench_rc=$?" >> gpurun_out/bench.log
+FORGE_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --steps 3 --no-breakdown > gpurun_out/bench2.log 2>&1; echo "bench2_rc=$?" >> gpurun_out/bench2.log
