@@ -129,10 +129,14 @@ static void gen_one(forge_op op, uint64_t u, uint64_t idx, int32_t variant, unsi
     case FORGE_OP_MV_MAT2_U32: {
       uint64_t u2 = orc_mix(u);
       forge_mat2_u32 v;
-      v.m[0] = (uint32_t)u;
-      v.m[1] = (uint32_t)(u >> 32);
-      v.m[2] = (uint32_t)u2;
-      v.m[3] = (uint32_t)(u2 >> 32);
+      /* odd diagonal, even off-diagonal: det is odd, so every prefix product
+         stays invertible mod 2^32 (uniform entries make long products collapse
+         to the zero matrix, and scans of them test nothing past the first
+         few hundred elements) */
+      v.m[0] = (uint32_t)u | 1u;
+      v.m[1] = (uint32_t)(u >> 32) & ~1u;
+      v.m[2] = (uint32_t)u2 & ~1u;
+      v.m[3] = (uint32_t)(u2 >> 32) | 1u;
       memcpy(out, &v, 16);
       break;
     }

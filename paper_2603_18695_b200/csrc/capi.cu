@@ -71,7 +71,8 @@ __global__ void fill_kernel(int op, unsigned char* dst, uint64_t n, uint64_t see
       }
       case FORGE_OP_MAT2_U32: case FORGE_OP_MV_MAT2_U32: {
         const uint64_t u2 = dmix(u);
-        forge::alg::Mat2 v{{uint32_t(u), uint32_t(u >> 32), uint32_t(u2), uint32_t(u2 >> 32)}};
+        // odd diagonal, even off-diagonal (invertible mod 2^32; oracle.c gen_one)
+        forge::alg::Mat2 v{{uint32_t(u) | 1u, uint32_t(u >> 32) & ~1u, uint32_t(u2) & ~1u, uint32_t(u2 >> 32) | 1u}};
         reinterpret_cast<forge::alg::Mat2*>(dst)[i] = v;
         break;
       }
