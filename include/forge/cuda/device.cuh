@@ -190,6 +190,16 @@ __device__ __forceinline__ void ld_relaxed_gpu_v2(const uint64_t* p, uint64_t& a
                : "l"(p)
                : "memory");
 }
+// 256-bit relaxed load (LDG.E.ENL2.256.STRONG.GPU): a 32-byte-aligned group
+// of tile states in one L2 sector request; each 64-bit element is
+// single-copy atomic on its own.
+__device__ __forceinline__ void ld_relaxed_gpu_v4(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c,
+                                                  uint64_t& d) {
+  asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p)
+               : "memory");
+}
 __device__ __forceinline__ void st_relaxed_gpu_v2(uint64_t* p, uint64_t a, uint64_t b) {
   asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
@@ -197,6 +207,11 @@ __device__ __forceinline__ void st_relaxed_gpu_v2(uint64_t* p, uint64_t a, uint6
 __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
   uint32_t r;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ uint64_t atom_add_acq_rel_gpu(uint64_t* p, uint64_t v) {
+  uint64_t r;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(v) : "memory");
   return r;
 }
 __device__ __forceinline__ uint32_t atom_add_relaxed_gpu(uint32_t* p, uint32_t v) {

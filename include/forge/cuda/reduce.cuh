@@ -50,6 +50,16 @@ struct CarryTraits {
 template <class S, class Op>
 struct CarryTraits<S, Op, std::void_t<typename Op::carry_traits>> : Op::carry_traits {};
 
+// kNarrowEmit (optional member of a wide carry policy): the scan's second pass
+// — the per-element running prefixes that become the outputs — runs in S,
+// started from the f64 exclusive prefix of the thread's row.  Aggregates and
+// carries stay in C, so no rounding accumulates across tiles; each output
+// carries only the ~(row length) f32 roundings of its own row.
+template <class CT, class = void>
+struct NarrowEmit : std::false_type {};
+template <class CT>
+struct NarrowEmit<CT, std::void_t<decltype(CT::kNarrowEmit)>> : std::bool_constant<CT::kNarrowEmit> {};
+
 // Arithmetic of one scan / ordered reduction: values of type A live in
 // registers and shared memory; lift() maps f's S result in, lower() maps out,
 // to_c()/from_c() cross into the carry type.
@@ -58,6 +68,7 @@ struct ScanMath {
   using CT = CarryTraits<S, Op>;
   using C = typename CT::C;
   using A = S;
+  static constexpr bool kNarrowEmit = false;
   static __device__ __forceinline__ A lift(const S& s) { return s; }
   static __device__ __forceinline__ S lower(const A& a) { return a; }
   static __device__ __forceinline__ A comb(const Op& o, const A& x, const A& y) { return o(x, y); }
@@ -70,6 +81,7 @@ struct ScanMath<S, Op, true> {
   using CT = CarryTraits<S, Op>;
   using C = typename CT::C;
   using A = C;
+  static constexpr bool kNarrowEmit = NarrowEmit<CT>::value;
   static __device__ __forceinline__ A lift(const S& s) { return CT::to_c(s); }
   static __device__ __forceinline__ S lower(const A& a) { return CT::to_s(a); }
   static __device__ __forceinline__ A comb(const Op& o, const A& x, const A& y) { return CT::op(o, x, y); }

@@ -50,7 +50,6 @@ namespace forge::cuda {
 
 constexpr int kScanThreads = 256;
 constexpr uint32_t kPartial = 1, kPrefix = 2;
-constexpr int kLookbackRows = 1;          // warp look-back: rows of 32 predecessors per round trip
 constexpr uint32_t kStateSlotWords = 32;  // 256-byte tile-state slots
 constexpr int kRowBytes = 128;            // smem kernel: bytes of T per thread row
 constexpr uint32_t kLookbackSkipProbe = 99;  // FORGE_DEV builds only: FORGE_SCAN_LOOKBACK=99 skips the look-back
@@ -62,16 +61,30 @@ constexpr int next_pow2(int v) {
   return p;
 }
 
+// Tile-state words.  Every 32-bit chunk of a published carry travels in its
+// own 64-bit word {tag, chunk}, tag = (epoch << 2) | kind; a state is accepted
+// only when all its words carry the same tag.  States are grouped P to a
+// 32-byte sector (P = 4 / 2 / 1 for 1 / 2 / 4-word states) and the groups sit
+// one per `stride`-word slot (256 bytes at full speed): one 256-bit load by a
+// look-back lane reads P consecutive tiles, so a warp's poll round covers 32 * P
+// predecessors for the same 32 L2 sector requests.
 template <class C>
 struct TileStateIO {
-  static constexpr int SW = Words<C>::N;  // 32-bit chunks of the carry
+  static constexpr int SW = Words<C>::N;        // 32-bit chunks of the carry
   static constexpr int STRIDE = next_pow2(SW);  // 64-bit words per state: every chunk, any sizeof(C)
+  static constexpr int P = STRIDE <= 4 ? 4 / STRIDE : 1;  // tiles per 32-byte group
+  static constexpr int GW = STRIDE * P;                   // 64-bit words per group (>= 4)
+
+  static __device__ __forceinline__ uint64_t* at(uint64_t* states, uint64_t tile, uint32_t stride) {
+    return states + (tile / P) * stride + (tile % P) * STRIDE;
+  }
+  static __host__ __device__ constexpr uint64_t slots(uint64_t tiles) { return (tiles + P - 1) / P; }
 
   static __device__ __forceinline__ void write(uint64_t* states, uint64_t tile, uint32_t stride,
                                                uint32_t epoch, uint32_t kind, const C& v) {
     Words<C> w = to_words(v);
     const uint64_t hi = uint64_t((epoch << 2) | kind) << 32;
-    uint64_t* p = states + tile * stride;
+    uint64_t* p = at(states, tile, stride);
     if constexpr (STRIDE == 1) {
       st_relaxed_gpu(p, hi | w.w[0]);
     } else {
@@ -84,19 +97,15 @@ struct TileStateIO {
     }
   }
 
-  // Split read for callers that poll many states at once: issue every load
-  // first (load_raw), decode after — so the loads are in flight together.
-  static __device__ __forceinline__ void load_raw(const uint64_t* states, uint64_t tile, uint32_t stride,
-                                                  uint64_t (&raw)[STRIDE]) {
-    const uint64_t* p = states + tile * stride;
-    if constexpr (STRIDE == 1) {
-      raw[0] = ld_relaxed_gpu(p);
-    } else {
+  // The whole group of slot `slot` (P tile states), 256-bit loads.
+  static __device__ __forceinline__ void load_group(const uint64_t* states, uint64_t slot, uint32_t stride,
+                                                    uint64_t (&raw)[GW]) {
+    const uint64_t* p = states + slot * stride;
 #pragma unroll
-      for (int i = 0; i < STRIDE; i += 2) ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
-    }
+    for (int i = 0; i < GW; i += 4) ld_relaxed_gpu_v4(p + i, raw[i], raw[i + 1], raw[i + 2], raw[i + 3]);
   }
-  static __device__ __forceinline__ uint32_t decode(const uint64_t (&raw)[STRIDE], uint32_t epoch, C& v,
+  // Decodes the state at word offset `off` of a group; 0 = INVALID.
+  static __device__ __forceinline__ uint32_t decode(const uint64_t* raw, uint32_t epoch, C& v,
                                                    uint32_t epoch_mask = 0x3fffffffu) {
     const uint32_t hi = uint32_t(raw[0] >> 32);
     bool same = true;
@@ -124,7 +133,7 @@ struct ScanArgs {
   const S* carry_in;  // nullable, device
   S* total_out;       // nullable, device
   uint64_t* states;   // tile states, state_stride words apart
-  uint32_t* ctrl;     // [0] ticket, [2] epoch
+  uint32_t* ctrl;     // 64-bit control word: {epoch (high 32), ticket (low 32)}
   uint32_t ntiles;
   uint32_t state_stride;  // 64-bit words per tile state slot
   uint32_t lookback;      // 0 (FORGE_DEV builds: kLookbackSkipProbe skips the look-back)
@@ -161,7 +170,8 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 // Phase timestamps of a tile: 0 claimed, 1 data landed, 2 pass 1 done,
-// 3 prefix known (look-back done), 4 pass 2 done; 5 = SM id.
+// 3 prefix known (look-back done), 4 pass 2 done; 5 = SM id, 6 = look-back
+// rounds, 7 = CTA start (before the speculative TMA and the claim).
 __device__ __forceinline__ void trace_mark(uint64_t* trace, uint64_t tile, int phase) {
   if (trace && threadIdx.x == 0) trace[tile * 8 + phase] = global_ns();
 }
@@ -177,88 +187,86 @@ struct ScanShared {
 template <class S, class Op>
 using ScanSharedOf = ScanShared<typename ScanMath<S, Op>::A, typename ScanMath<S, Op>::C>;
 
-// Decoupled look-back by one warp (primitives.hpp:536-576), Q rows of 32
-// predecessors per L2 round trip: every lane issues its Q state loads together
-// (decode after issue, so they are in flight at once), re-polls only the
-// positions still INVALID, then finds the nearest PREFIX with one ballot per
-// row and folds everything newer than it with an ORDER-PRESERVING log-step
-// reduction (older tile always on the left; the reference folded serially,
-// :561-563).  Returns the carry (all lanes).
-// Measured (tools/trace_scan.py, f32 2^28): the nearest PREFIX sits ~100 tiles
-// back under load; Q = 1 takes 3.4 rounds of 1.65 us, Q = 4 takes 2.0 rounds of
-// 3.5 us — a round's latency grows with the polls because ~800 resident tiles
-// poll the same few hundred newest state lines — so Q = 1 stays the default.
-template <int Q, class IO, class C, class COp>
+// Decoupled look-back by one warp (primitives.hpp:536-576).  Each round, lane
+// l reads state group (top - l) with one 256-bit load — P consecutive tiles —
+// re-polls only while its group holds an INVALID state newer than its newest
+// PREFIX, and pre-folds its group newest-to-oldest (stopping at a PREFIX).
+// One ballot then finds the nearest lane holding a PREFIX and the lanes newer
+// than it are folded with an ORDER-PRESERVING log-step reduction (older
+// always on the left; the reference folded serially, :561-563).  Returns the
+// carry (all lanes).
+// Measured (tools/trace_scan.py, f32 2^28, one tile per lane): the nearest
+// PREFIX sits ~100 tiles back under load and a poll round costs 1.7-3 us
+// (tools/probe_rtt.cu: L2-hit latency under full HBM streaming), so the
+// window per round, not the number of loads, sets the look-back time.
+template <class IO, class C, class COp>
 __device__ __forceinline__ Opt<C> warp_lookback(const uint64_t* states, uint32_t stride, uint32_t epoch,
                                                 int64_t tile, const COp& cop, uint64_t* trace, uint64_t trace_tile,
                                                 uint32_t backoff_ns, uint32_t epoch_mask) {
-  constexpr uint32_t kEmpty = 4;  // position before tile 0
+  constexpr uint32_t kEmpty = 4;  // group before tile 0
+  constexpr int P = IO::P;
   const unsigned lane = lane_id();
   Opt<C> carry{C{}, false};
-  int64_t hi = tile;
+  int64_t top = (tile - 1) / P;  // group of the newest predecessor
   uint32_t rounds = 0;
   for (;;) {
     ++rounds;
-    C val[Q];
-    uint32_t kind[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      kind[q] = hi - 1 - int64_t(q * kWarp + lane) < 0 ? kEmpty : 0u;
-      val[q] = C{};
-    }
+    const int64_t slot = top - int64_t(lane);
+    uint32_t kind = slot < 0 ? kEmpty : 0u;  // lane summary: PARTIAL / PREFIX / kEmpty; 0 = re-poll
+    Opt<C> val{C{}, false};
     for (;;) {
-      uint64_t raw[Q][IO::STRIDE];
+      if (kind == 0) {
+        uint64_t raw[IO::GW];
+        IO::load_group(states, uint64_t(slot), stride, raw);
+        Opt<C> acc{C{}, false};
+        uint32_t k = kPartial;
 #pragma unroll
-      for (int q = 0; q < Q; ++q)
-        if (kind[q] == 0) IO::load_raw(states, uint64_t(hi - 1 - int64_t(q * kWarp + lane)), stride, raw[q]);
-      bool all = true;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        if (kind[q] == 0) {
-          kind[q] = IO::decode(raw[q], epoch, val[q], epoch_mask);
-          all &= kind[q] != 0;
+        for (int q = P - 1; q >= 0; --q) {
+          if (k != kPartial || slot * P + q >= tile) continue;  // resolved, or not a predecessor
+          C v;
+          const uint32_t kq = IO::decode(raw + q * IO::STRIDE, epoch, v, epoch_mask);
+          if (kq == 0) {
+            k = 0;
+          } else {
+            acc = opt_combine(cop, Opt<C>{v, true}, acc);
+            if (kq == kPrefix) k = kPrefix;
+          }
         }
+        kind = k;
+        val = acc;
       }
-      if (__all_sync(kFullMask, all)) break;
+      if (__all_sync(kFullMask, kind != 0)) break;
       if (backoff_ns) __nanosleep(backoff_ns);
     }
-    int P = Q * kWarp;  // position of the nearest PREFIX (0 = tile hi-1)
+    const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
+    const int near = pm ? __ffs(int(pm)) - 1 : kWarp;  // lane of the nearest PREFIX (kWarp: none)
+    Opt<C> v{val.v, int(lane) <= near && kind != kEmpty && val.has};
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const unsigned pm = __ballot_sync(kFullMask, kind[q] == kPrefix);
-      if (P == Q * kWarp && pm) P = q * kWarp + __ffs(int(pm)) - 1;
+    for (unsigned d = 1; d < kWarp; d <<= 1) {
+      Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
+      if (lane + d < kWarp) v = opt_combine(cop, got, v);
     }
-    Opt<C> win{C{}, false};
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      if (q * kWarp <= P) {
-        Opt<C> v{val[q], int(q * kWarp + lane) <= P && kind[q] != kEmpty};
-#pragma unroll
-        for (unsigned d = 1; d < kWarp; d <<= 1) {
-          Opt<C> got{shfl_down(v.v, d), __shfl_down_sync(kFullMask, int(v.has), d) != 0};
-          if (lane + d < kWarp) v = opt_combine(cop, got, v);
-        }
-        win = opt_combine(cop, shfl_idx_opt(v, 0), win);  // row q is older than rows < q
-      }
-    }
-    carry = opt_combine(cop, win, carry);
-    if (P < Q * kWarp) break;
-    hi -= Q * kWarp;
+    carry = opt_combine(cop, shfl_idx_opt(v, 0), carry);
+    if (near < kWarp || top < kWarp) break;  // found a PREFIX, or reached tile 0
+    top -= kWarp;
   }
   if (trace && lane == 0) trace[trace_tile * 8 + 6] = rounds;
   return carry;
 }
 
-// Reads the epoch, claims the next tile (acq_rel ticket); the last of the
-// `ntiles` claims resets the ticket and advances the epoch (see header).
+// Claims the next tile: ONE 64-bit atomic on the control word {epoch:32,
+// ticket:32} returns the ticket and this launch's epoch together (one L2
+// round trip, ~2 us under full HBM load — a separate epoch load before the
+// ticket would be a second, serial one).  The last of the `ntiles` claims
+// resets the ticket and advances the epoch for the next launch; no CTA of this
+// launch touches the word after it.
 template <class T, class S, class F, class Op>
 __device__ __forceinline__ uint32_t claim_tile(const ScanArgs<T, S, F, Op>& a, uint32_t& epoch) {
-  epoch = ld_acquire_gpu(a.ctrl + 2);
-  const uint32_t t = atom_add_acq_rel_gpu(a.ctrl + 0, 1u);
-  if (t == a.ntiles - 1) {
-    st_relaxed_gpu(a.ctrl + 0, 0u);
-    st_relaxed_gpu(a.ctrl + 2, epoch + 1u);
-  }
+  uint64_t* word = reinterpret_cast<uint64_t*>(a.ctrl);
+  const uint64_t got = atom_add_acq_rel_gpu(word, uint64_t(1));
+  const uint32_t t = uint32_t(got);
+  epoch = uint32_t(got >> 32);
+  if (t == a.ntiles - 1) st_relaxed_gpu(word, uint64_t(epoch + 1u) << 32);
   return t;
 }
 
@@ -328,8 +336,8 @@ __device__ __forceinline__ void block_exclusive_prefix(
     if (a.lookback == kLookbackSkipProbe) {
       // development ceiling probe (FORGE_SCAN_LOOKBACK=99): no look-back, WRONG results
     } else if (warp == 0) {
-      carry = warp_lookback<kLookbackRows, IO, C>(a.states, a.state_stride, epoch, int64_t(tile), cop, a.trace, tile,
-                                                  a.backoff_ns, a.epoch_mask);
+      carry = warp_lookback<IO, C>(a.states, a.state_stride, epoch, int64_t(tile), cop, a.trace, tile, a.backoff_ns,
+                                   a.epoch_mask);
     }
     if (threadIdx.x == 0) {
       const C inclusive_c = cop(carry.v, agg_c);
@@ -496,6 +504,7 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
       tma_load_2d(tile_mem + size_t(r) * kSmemTileBytes, &tmap, 0, (int(t) * R + r) * kScanThreads, &bar);
   };
 
+  const uint64_t t_start = a.trace ? global_ns() : 0;
   if (threadIdx.x == 0) {
     // The tile to load is guessed as blockIdx.x and its TMA issued BEFORE the
     // ticket round trip (CTAs are dispatched in index order in practice); the
@@ -525,6 +534,7 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
     uint32_t sm;
     asm("mov.u32 %0, %%smid;" : "=r"(sm));
     a.trace[tile * 8 + 5] = sm;
+    a.trace[tile * 8 + 7] = t_start;
   }
   const bool full = (tile + 1) * kTile <= a.n;
   uint64_t base[R];
@@ -574,7 +584,36 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
   block_exclusive_prefix<R>(a, tile, s_epoch, tot, sh, run);
   trace_mark(a.trace, tile, 3);
 
-  // ---- pass 2: running prefixes, stored as they are produced
+  // ---- pass 2: running prefixes, stored as they are produced.  E is the
+  // type of the running value: A, or S for kNarrowEmit ops (the f64 exclusive
+  // prefix rounded once, then the row's items composed in S).
+  using E = std::conditional_t<M::kNarrowEmit, S, A>;
+  Opt<E> emit[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if constexpr (M::kNarrowEmit)
+      emit[r] = Opt<E>{M::lower(run[r].v), run[r].has};
+    else
+      emit[r] = run[r];
+  }
+  auto eop = [&](const E& x, const E& y) {
+    if constexpr (M::kNarrowEmit)
+      return a.op(x, y);
+    else
+      return aop(x, y);
+  };
+  auto elift = [&](const S& y) {
+    if constexpr (M::kNarrowEmit)
+      return y;
+    else
+      return M::lift(y);
+  };
+  auto elower = [&](const E& v) {
+    if constexpr (M::kNarrowEmit)
+      return v;
+    else
+      return M::lower(v);
+  };
   if (full) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -588,15 +627,15 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
         S o[EPC];
 #pragma unroll
         for (int e = 0; e < EPC; ++e) {
-          const A y = M::lift(a.f(x[e]));
+          const E y = elift(a.f(x[e]));
           if constexpr (Inclusive) {
-            run[r].v = run[r].has ? aop(run[r].v, y) : y;
-            run[r].has = true;
-            o[e] = M::lower(run[r].v);
+            emit[r].v = emit[r].has ? eop(emit[r].v, y) : y;
+            emit[r].has = true;
+            o[e] = elower(emit[r].v);
           } else {
-            o[e] = run[r].has ? M::lower(run[r].v) : a.identity;
-            run[r].v = run[r].has ? aop(run[r].v, y) : y;
-            run[r].has = true;
+            o[e] = emit[r].has ? elower(emit[r].v) : a.identity;
+            emit[r].v = emit[r].has ? eop(emit[r].v, y) : y;
+            emit[r].has = true;
           }
         }
         if constexpr (sizeof(S) == sizeof(T)) {
@@ -634,15 +673,15 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       for (int k = 0; k < count[r]; ++k) {
-        const A y = M::lift(a.f(a.src[base[r] + k]));
+        const E y = elift(a.f(a.src[base[r] + k]));
         if constexpr (Inclusive) {
-          run[r].v = run[r].has ? aop(run[r].v, y) : y;
-          run[r].has = true;
-          a.dst[base[r] + k] = M::lower(run[r].v);
+          emit[r].v = emit[r].has ? eop(emit[r].v, y) : y;
+          emit[r].has = true;
+          a.dst[base[r] + k] = elower(emit[r].v);
         } else {
-          a.dst[base[r] + k] = run[r].has ? M::lower(run[r].v) : a.identity;
-          run[r].v = run[r].has ? aop(run[r].v, y) : y;
-          run[r].has = true;
+          a.dst[base[r] + k] = emit[r].has ? elower(emit[r].v) : a.identity;
+          emit[r].v = emit[r].has ? eop(emit[r].v, y) : y;
+          emit[r].has = true;
         }
       }
     }
@@ -653,35 +692,38 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
 // ---------------------------------------------------------------------------
 // Workspace + launch.
 
-// Workspace: [256-byte control block (ticket, epoch) | one state slot per tile].
-// Full-speed slots are 256 bytes (kSlotWords); a smaller
-// workspace is accepted down to packed slots (kMinSlotWords) at some look-back
-// speed.  The size depends on S only, so a workspace made for S
-// (make_scan_workspace<S>) fits every T: the bound is the larger of the
-// general kernel's tiles (256 x 64 bytes of S) at packed slots and the smem
-// kernel's tiles of a sizeof(S)-byte T at full slots.
+// Workspace: [256-byte control block (ticket, epoch) | one slot per group of
+// P tile states (TileStateIO)].  Full-speed slots are 256 bytes (kSlotWords,
+// DESIGN.md §4); a smaller workspace is accepted down to packed groups
+// (kMinSlotWords = one 32-byte group) at some look-back speed.  The size
+// depends on S only, so a workspace made for S (make_scan_workspace<S>) fits
+// every T: the bound is the larger of the general kernel's tiles (256 x 64
+// bytes of S) at packed groups and the smem kernel's tiles of a
+// sizeof(S)-byte T at full slots.
 template <class T, class S, class Op>
 struct ScanWs {
   using C = typename CarryTraits<S, Op>::C;
+  using IO = TileStateIO<C>;
   static constexpr uint64_t kTileGeneral = uint64_t(kScanThreads) * scan_items<S>();
-  static constexpr uint32_t kMinSlotWords = uint32_t(TileStateIO<C>::STRIDE);
+  static constexpr uint32_t kMinSlotWords = uint32_t(IO::GW);
   static constexpr uint32_t kSlotWords = kMinSlotWords > kStateSlotWords ? kMinSlotWords : kStateSlotWords;
   static constexpr uint64_t kSizedTile =  // smem tile of a T with sizeof(T) == sizeof(S)
       sizeof(S) >= 16 ? 2 * uint64_t(kScanThreads) * (kRowBytes / 16)
                       : uint64_t(kScanThreads) * (sizeof(S) <= uint64_t(kRowBytes) ? kRowBytes / sizeof(S) : 1);
-  static uint64_t min_bytes_for(uint64_t tiles) { return 256 + (tiles ? tiles : 1) * kMinSlotWords * 8; }
+  static uint64_t min_bytes_for(uint64_t tiles) { return 256 + IO::slots(tiles ? tiles : 1) * kMinSlotWords * 8; }
   static uint64_t bytes(uint64_t n) {
-    const uint64_t full = 256 + (n ? ceil_div(n, kSizedTile) : 1) * kSlotWords * 8;
+    const uint64_t full = 256 + IO::slots(n ? ceil_div(n, kSizedTile) : 1) * kSlotWords * 8;
     const uint64_t packed = min_bytes_for(ceil_div(n, kTileGeneral));
     return full > packed ? full : packed;
   }
   // Largest slot stride (64-bit words, power of two, <= kSlotWords) that fits
-  // `tiles` slots in `ws_bytes`; 0 when even packed slots do not fit.
+  // the groups of `tiles` tiles in `ws_bytes`; 0 when even packed groups do not fit.
   static uint32_t slot_words(uint64_t tiles, uint64_t ws_bytes) {
     for (uint32_t w = kSlotWords; w >= kMinSlotWords && w > 0; w >>= 1)
-      if (256 + (tiles ? tiles : 1) * uint64_t(w) * 8 <= ws_bytes) return w;
+      if (256 + IO::slots(tiles ? tiles : 1) * uint64_t(w) * 8 <= ws_bytes) return w;
     return 0;
   }
+  static uint64_t claim_bytes(uint64_t tiles, uint32_t stride) { return 256 + IO::slots(tiles) * stride * 8; }
 };
 
 // Development knobs (FORGE_DEV builds only; constants otherwise).
@@ -786,7 +828,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
 #ifdef FORGE_DEV
       a.trace = scan_trace_for(a.ntiles);
 #endif
-      if (const cudaError_t e = ws_claim(ws, kWsTagScan, 256 + uint64_t(a.ntiles) * a.state_stride * 8, stream);
+      if (const cudaError_t e = ws_claim(ws, kWsTagScan, WsT::claim_bytes(a.ntiles, a.state_stride), stream);
           e != cudaSuccess)
         return e;
       CUtensorMap tmap_out = tmap;
@@ -799,7 +841,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   a.ntiles = uint32_t(ceil_div(n, WsT::kTileGeneral));
   a.state_stride = WsT::slot_words(a.ntiles, ws_bytes);
   if (a.state_stride == 0) return cudaErrorInvalidValue;
-  if (const cudaError_t e = ws_claim(ws, kWsTagScan, 256 + uint64_t(a.ntiles) * a.state_stride * 8, stream);
+  if (const cudaError_t e = ws_claim(ws, kWsTagScan, WsT::claim_bytes(a.ntiles, a.state_stride), stream);
       e != cudaSuccess)
     return e;
   if (inclusive)

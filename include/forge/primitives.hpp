@@ -267,13 +267,20 @@ inline uint64_t b200_state_min_bytes(uint32_t accum_size) {  // packed slot: eve
   while (stride < words) stride <<= 1;
   return stride * 8;
 }
+inline uint64_t b200_state_group_tiles(uint32_t accum_size) {  // tile states per 32-byte group
+  const uint64_t words = b200_state_min_bytes(accum_size) / 8;
+  return words <= 4 ? 4 / words : 1;
+}
 inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
-  const uint64_t full = 256 + std::max<uint64_t>((n + b200_scan_sized_tile(accum_size) - 1) /
-                                                     b200_scan_sized_tile(accum_size), 1) *
-                                  std::max<uint64_t>(b200_state_min_bytes(accum_size), 256);
-  const uint64_t packed = 256 + std::max<uint64_t>((n + b200_scan_general_tile(accum_size) - 1) /
-                                                       b200_scan_general_tile(accum_size), 1) *
-                                    b200_state_min_bytes(accum_size);
+  const uint64_t P = b200_state_group_tiles(accum_size);
+  const uint64_t sized_tiles = std::max<uint64_t>((n + b200_scan_sized_tile(accum_size) - 1) /
+                                                      b200_scan_sized_tile(accum_size), 1);
+  const uint64_t full = 256 + (sized_tiles + P - 1) / P *
+                                  std::max<uint64_t>(b200_state_min_bytes(accum_size) * P, 256);
+  const uint64_t packed = 256 + 32 +  // + one partial 32-byte group
+                          std::max<uint64_t>((n + b200_scan_general_tile(accum_size) - 1) /
+                                                 b200_scan_general_tile(accum_size), 1) *
+                              b200_state_min_bytes(accum_size);
   return std::max(full, packed);
 }
 inline uint64_t b200_sm_count() {

@@ -486,4 +486,14 @@ int forge_dev_fill_synthetic(forge_op op, void* dst, uint64_t n, uint64_t seed, 
   });
 }
 
+#ifdef FORGE_DEV
+// Development build only (make DEV=1): the per-tile phase trace of the last
+// scan run with FORGE_SCAN_TRACE=1 (tools/trace_scan.py), 8 words per tile.
+int forge_dev_scan_trace(void** ptr, uint64_t* words) {
+  *ptr = cuda::scan_trace_buffer();
+  *words = cuda::scan_trace_words();
+  return FORGE_OK;
+}
+#endif
+
 }  // extern "C"

@@ -18,6 +18,10 @@ namespace forge::menu {
 
 using namespace forge::alg;
 
+#ifndef FORGE_AFFINE_NARROW_EMIT
+#define FORGE_AFFINE_NARROW_EMIT 1
+#endif
+
 // ---- carry policies
 struct F32SumCarry {
   using C = double;
@@ -30,7 +34,8 @@ struct F32SumCarry {
 
 struct AffineCarry {
   using C = AffineT<double>;
-  static constexpr bool kWide = true;  // product chain: whole scan in f64
+  static constexpr bool kWide = true;        // product chain: aggregates and carries in f64 ...
+  static constexpr bool kNarrowEmit = FORGE_AFFINE_NARROW_EMIT;  // ... per-row output prefixes in f32
   static __device__ __forceinline__ C to_c(const Affine& s) { return C{double(s.a), double(s.b)}; }
   static __device__ __forceinline__ Affine to_s(const C& c) { return Affine{float(c.a), float(c.b)}; }
   template <class Op>

@@ -74,13 +74,15 @@ def test_descriptor_literals():
 def test_arch_params_defaults_and_workspace_sizing():
     p = F.ArchParams()
     assert (p.warp_width, p.mapreduce_blocks, p.threads_per_block, p.nitem_scan) == (32, 100, 256, 16)
-    # B200 workspace sizes: 256-byte control block + one 256-byte state slot per
-    # 8192-f32 tile of the smem kernel (full speed); never less than the general
-    # kernel's 4096-element tiles at packed 16-byte states (the f64 carry)
+    # B200 workspace sizes: 256-byte control block + one 256-byte slot per
+    # 32-byte group of two 16-byte tile states (the f64 carry of an f32 sum) —
+    # two 8192-f32 tiles of the smem kernel (full speed); never less than the
+    # general kernel's 4096-element tiles at packed 16-byte states
     assert F.required_workspace(capi.PRIM_SCAN, 4, 4096) == 256 + 256
     assert F.required_workspace(capi.PRIM_SCAN, 4, 8192) == 256 + 256
-    assert F.required_workspace(capi.PRIM_SCAN, 4, 8193) == 256 + 512
-    assert F.required_workspace(capi.PRIM_SCAN, 4, 1 << 33) == 256 + (1 << 20) * 256
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 16384) == 256 + 256
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 16385) == 256 + 512
+    assert F.required_workspace(capi.PRIM_SCAN, 4, 1 << 33) == 256 + (1 << 19) * 256
     assert F.required_workspace(capi.PRIM_VCOPY, 4, 100) == 0
     # the reference-facing bound covers the device layer's need for every menu op
     # (a workspace made for S fits every T: ADVICE r01)
