@@ -297,6 +297,11 @@ struct LogSumExp {
   FORGE_HD F operator()(F a, F b) const { return log_sum_exp(a, b); }
 };
 struct DecodeUF8 {
+  // decode is affine in the code: -1 + (2/255) c.  Mapreduce with a real sum
+  // may fold the codes exactly as integers (forge/cuda/reduce.cuh code sums).
+  static constexpr bool kAffineCode = true;
+  static constexpr double kCodeOffset = -1.0;
+  static constexpr double kCodeScale = 2.0 / 255.0;
   FORGE_HD float operator()(UnitFloat8 c) const { return decode(c); }
 };
 

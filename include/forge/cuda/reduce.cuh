@@ -361,10 +361,132 @@ inline uint32_t mapreduce_grid(uint64_t n) {
   return uint32_t(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
+// ---------------------------------------------------------------------------
+// Exact code sums.  A one-byte map that is affine in the code, f(c) = off +
+// scale * c (e.g. UnitFloat8 decode = -1 + 2c/255, algebra.hpp:15-28), folded
+// with a real-number sum: the result is n * off + scale * SUM(c), and SUM(c) is
+// an exact integer — IDP4A (4 codes per instruction against 0x01010101) into
+// 32-bit lane sums, flushed to 64 bits per pass.  One IDP4A per 4 input bytes
+// instead of a table lookup + FADD per byte: the read roof at 1 byte per
+// element.  The result is the real-number value of the sum rounded once; the
+// tabulated path rounds each decoded term and the running sum instead
+// (both within the f32 parity bar; the exact sum is the more accurate).
+//
+// A map opts in with `static constexpr bool kAffineCode = true;` plus
+// kCodeOffset / kCodeScale; an op with `static constexpr bool kRealSum = true;`.
+template <class F, class = void>
+struct AffineCodeMap : std::false_type {};
+template <class F>
+struct AffineCodeMap<F, std::void_t<decltype(F::kAffineCode)>> : std::bool_constant<F::kAffineCode> {};
+template <class Op, class = void>
+struct RealSumOp : std::false_type {};
+template <class Op>
+struct RealSumOp<Op, std::void_t<decltype(Op::kRealSum)>> : std::bool_constant<Op::kRealSum> {};
+
+template <class T, class S, class F, class Op>
+constexpr bool code_sum_ok() {
+  return sizeof(T) == 1 && (std::is_same_v<S, float> || std::is_same_v<S, double>) && AffineCodeMap<F>::value &&
+         RealSumOp<Op>::value;
+}
+
+constexpr int kCodeSumUnroll = 4;  // 4 x 32 bytes in flight per thread
+
+template <class S>
+__global__ void __launch_bounds__(kReduceThreads)
+    code_sum_kernel(const uint8_t* __restrict__ src, uint64_t n, double off, double scale,
+                    unsigned long long* partials, uint32_t* ticket, S* out, uint32_t* out_has) {
+  constexpr uint64_t kChunk = uint64_t(kReduceThreads) * kCodeSumUnroll;  // 32-byte vectors per chunk
+  __shared__ unsigned long long smem[kReduceThreads / kWarp];
+  __shared__ bool s_last;
+  const uint64_t gtid = uint64_t(blockIdx.x) * kReduceThreads + threadIdx.x;
+  const uint64_t gsize = uint64_t(gridDim.x) * kReduceThreads;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(src);
+  uint64_t head = (32 - addr % 32) % 32;
+  if (head > n) head = n;
+  const uint64_t nvec = (n - head) / 32;
+  const uint8_t* body = src + head;
+  unsigned long long total = 0;
+  auto sum32 = [](const uint32_t (&w)[8], uint32_t acc) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = __dp4a(w[k], 0x01010101u, acc);
+    return acc;
+  };
+  const uint64_t full = nvec / kChunk;
+  for (uint64_t c = blockIdx.x; c < full; c += gridDim.x) {
+    uint32_t w[kCodeSumUnroll][8];
+#pragma unroll
+    for (int u = 0; u < kCodeSumUnroll; ++u)
+      load_items<uint32_t, 8>(reinterpret_cast<const uint32_t*>(body + (c * kChunk + u * kReduceThreads + threadIdx.x) * 32),
+                              w[u]);
+    uint32_t acc = 0;  // <= 4 * 8 * 1020: no overflow
+#pragma unroll
+    for (int u = 0; u < kCodeSumUnroll; ++u) acc = sum32(w[u], acc);
+    total += acc;
+  }
+  for (uint64_t v = full * kChunk + gtid; v < nvec; v += gsize) {
+    uint32_t w[8];
+    load_items<uint32_t, 8>(reinterpret_cast<const uint32_t*>(body + v * 32), w);
+    total += sum32(w, 0u);
+  }
+  const uint64_t tail0 = head + nvec * 32;
+  const uint64_t extra = head + (n - tail0);
+  for (uint64_t e = gtid; e < extra; e += gsize) total += src[e < head ? e : tail0 + (e - head)];
+
+  // block sum, then the last block to arrive folds the partials
+  auto block_sum = [&](unsigned long long v) {
+#pragma unroll
+    for (int d = kWarp / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(kFullMask, v, d);
+    if (lane_id() == 0) smem[threadIdx.x / kWarp] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+      for (int w = 0; w < kReduceThreads / kWarp; ++w) t += smem[w];
+    __syncthreads();
+    return t;
+  };
+  const unsigned long long blk = block_sum(total);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = blk;
+    const uint32_t t = atom_add_acq_rel_gpu(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) st_relaxed_gpu(ticket, 0u);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  unsigned long long v = 0;
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kReduceThreads) v += ld_strong(partials + b);
+  const unsigned long long codes = block_sum(v);
+  if (threadIdx.x == 0) {
+    *out = S(off * double(n) + scale * double(codes));
+    if (out_has) *out_has = n > 0 ? 1u : 0u;
+  }
+}
+
+template <class S>
+cudaError_t launch_code_sum(const uint8_t* src, uint64_t n, double off, double scale, S* out_dev,
+                            uint32_t* out_has_dev, void* ws, cudaStream_t stream) {
+  const uint32_t grid = mapreduce_grid<uint32_t>(ceil_div(n, 4));
+  uint32_t* ticket;
+  S* parts_s;
+  uint32_t* has;
+  MapReduceWs<S>::carve(ws, mapreduce_max_grid(), ticket, parts_s, has);
+  // 64-bit partials span the partial and flag areas (>= 8 bytes per block)
+  static_assert(sizeof(S) >= 4, "code sums carve 8 bytes per block from S partials + flags");
+  auto* parts = reinterpret_cast<unsigned long long*>(parts_s);
+  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream); e != cudaSuccess) return e;
+  code_sum_kernel<S><<<grid, kReduceThreads, 0, stream>>>(src, n, off, scale, parts, ticket, out_dev, out_has_dev);
+  return cudaGetLastError();
+}
+
 // Launch; `ws` holds MapReduceWs<S>::bytes(mapreduce_max_grid()) zero-initialised bytes.
 template <class T, class S, class F, class Op>
 cudaError_t launch_mapreduce(const T* src, uint64_t n, uint64_t stride, const F& f, const Op& op,
                              S* out_dev, uint32_t* out_has_dev, void* ws, cudaStream_t stream) {
+  if constexpr (code_sum_ok<T, S, F, Op>()) {
+    if (stride == 1 && n > 0)
+      return launch_code_sum<S>(reinterpret_cast<const uint8_t*>(src), n, double(F::kCodeOffset),
+                                double(F::kCodeScale), out_dev, out_has_dev, ws, stream);
+  }
   const uint32_t grid = mapreduce_grid<T>(stride == 1 ? n : n * 4);
   MapReduceArgs<T, S, F, Op> a{src, n, stride, f, op, nullptr, nullptr, nullptr, out_dev, out_has_dev};
   MapReduceWs<S>::carve(ws, mapreduce_max_grid(), a.ticket, a.partials, a.part_has);

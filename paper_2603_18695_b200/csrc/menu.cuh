@@ -71,6 +71,7 @@ struct LseCarry {
 // ---- operators
 struct AddF32 {
   using carry_traits = F32SumCarry;
+  static constexpr bool kRealSum = true;  // a real-number sum (code sums may fold exactly)
   FORGE_HD float operator()(float a, float b) const { return a + b; }
 };
 struct AddF64 {

@@ -349,6 +349,18 @@ void test_vcopy_struct(Machine& m) {
 struct Half {  // u8 -> f32: x / 2 (exact)
   FORGE_HD float operator()(uint8_t c) const { return 0.5f * float(c); }
 };
+// A map affine in the code plus a real-number sum: mapreduce takes the exact
+// integer code-sum path (IDP4A, forge/cuda/reduce.cuh) for these.
+struct Centered {  // u8 -> f32: (c - 127.5) / 4
+  static constexpr bool kAffineCode = true;
+  static constexpr double kCodeOffset = -127.5 / 4.0;
+  static constexpr double kCodeScale = 0.25;
+  FORGE_HD float operator()(uint8_t c) const { return 0.25f * (float(c) - 127.5f); }
+};
+struct RealPlusF32 {
+  static constexpr bool kRealSum = true;
+  FORGE_HD float operator()(float a, float b) const { return a + b; }
+};
 struct Widen16 {  // u16 -> i32
   FORGE_HD int32_t operator()(uint16_t c) const { return int32_t(c); }
 };
@@ -395,6 +407,17 @@ void test_mixed_width_maps(Machine& m) {
     for (uint8_t c : x8) want += 0.5 * c;
     EXPECT(r.ok && std::abs(double(rf) - want) <= 1e-5 * want, "u8->f32 mapreduce n=%llu: %.9g vs %.9g",
            (unsigned long long)n, rf, want);
+    // exact code sums (affine map + real sum), aligned and misaligned (head/tail bytes) views
+    auto s_c = make_semiring<float>(Centered{}, RealPlusF32{}, std::optional<float>(0.f), true);
+    for (uint64_t off : {0ull, 3ull}) {
+      if (off >= n) continue;
+      float rc = 0;
+      r = prim::mapreduce(m, s_c, intr::make_view<uint8_t>(m, b8).strided(off, n - off, 1), wf, p, &rc);
+      double ex = 0, sc = 0;
+      for (uint64_t i = off; i < n; ++i) ex += 0.25 * (double(x8[i]) - 127.5), sc += std::abs(0.25 * (double(x8[i]) - 127.5));
+      EXPECT(r.ok && std::abs(double(rc) - ex) <= 1e-5 * sc + 1e-30, "u8 code-sum mapreduce n=%llu off=%llu: %.9g vs %.9g",
+             (unsigned long long)n, (unsigned long long)off, rc, ex);
+    }
     // u16 -> i32 wrapping sum, u16 max
     auto s_w = make_semiring<int32_t>(Widen16{}, alg::WrapPlusI32{}, std::optional<int32_t>(0), true);
     prim::Workspace wi = prim::make_mapreduce_workspace<int32_t>(m, p);
