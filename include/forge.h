@@ -357,6 +357,67 @@ int forge_dev_copy(const void* src, void* dst, uint64_t bytes, void* stream);
 int forge_dev_fill_synthetic(forge_op op, void* dst, uint64_t n, uint64_t seed,
                              uint64_t index_base, int32_t variant, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Single-process multi-GPU sharding for C / C++ callers.
+ * The reference has no multi-device layer (one Machine = one simulated device,
+ * machine.hpp:139-141); these calls shard the primitives across the GPUs of
+ * one node, one shard per device, shards in rank order.
+ *
+ * forge_group_create(devices, count): count ordinals, rank r on devices[r].
+ *   All distinct -> an NCCL clique (ncclCommInitAll over NVLink / NVSwitch;
+ *   libnccl.so.2 is opened at first use, FORGE_ERR_UNSUPPORTED without it).
+ *   All the same -> an EMULATED group: G shards on one GPU running the same
+ *   exchange logic, the all-gather done by device copies (1-GPU test boxes).
+ *   Anything else -> InvalidArgument.  The group owns one stream per shard;
+ *   the sharded calls are stream-ordered on those streams (no host sync,
+ *   except forge_sharded_mapreduce's host result) — forge_group_synchronize
+ *   waits for them.  One group serves one sharded call at a time.
+ *
+ * Arrays are indexed by rank: src[r] / dst[r] / ws[r] are device pointers on
+ * shard r's device, ws_bytes[r] >= forge_dev_workspace_bytes for that shard.
+ * Shard r of a length-`total` array is forge_shard_range(total, r, G). */
+typedef struct forge_group forge_group;
+
+int forge_shard_range(uint64_t total, int32_t rank, int32_t count, uint64_t* lo, uint64_t* hi);
+int forge_group_create(const int32_t* devices, int32_t count, forge_group** out);
+int forge_group_destroy(forge_group* g);
+int forge_group_size(forge_group* g, int32_t* count, int32_t* emulated);
+int forge_group_stream(forge_group* g, int32_t rank, void** stream);
+int forge_group_synchronize(forge_group* g);
+
+/* mapreduce (primitives.hpp:348-351) of the concatenation of the shards
+ * src[r][0..n[r]): local one-kernel mapreduce per shard, all-gather of the G
+ * partials, rank-order fold on every device.  *result_host (nullable) gets the
+ * S value (synchronous readback from rank 0); forge_sharded_result_dev gives
+ * each shard's device copy. */
+int forge_sharded_mapreduce(forge_group* g, forge_op op, const void* const* src, const uint64_t* n,
+                            void* const* ws, const uint64_t* ws_bytes, void* result_host);
+int forge_sharded_result_dev(forge_group* g, int32_t rank, void** value_dev);
+
+/* scan (primitives.hpp:440-443) of the concatenation of the shards: dst[r]
+ * receives shard r's slice of the global scan.  Reduce-then-scan: ordered shard
+ * totals, all-gather, exclusive rank-order fold into a device carry, carry-
+ * seeded single-pass scan.  ws_bytes[r] must cover both the PRIM_SCAN and the
+ * PRIM_MAPREDUCE workspace of shard r (the shard total is reduced with it). */
+int forge_sharded_scan(forge_group* g, forge_op op, int32_t inclusive, const void* const* src,
+                       void* const* dst, const uint64_t* n, void* const* ws, const uint64_t* ws_bytes);
+
+/* matvec / gevm (primitives.hpp:776-791) of a global n x p column-major A,
+ * COLUMNS sharded: A_blocks[r] is shard r's n x p_r column block (p_r from
+ * forge_shard_range(p_cols, r, G)), x[r] the full length-n x on shard r,
+ * y_blocks[r] its p_r outputs.  No collective. */
+int forge_sharded_matvec(forge_group* g, forge_op op, const void* const* A_blocks, uint64_t n,
+                         uint64_t p_cols, const void* const* x, void* const* y_blocks, void* const* ws,
+                         const uint64_t* ws_bytes);
+
+/* vecmat / gemv (primitives.hpp:795-807), ROWS sharded: A_blocks[r] is shard
+ * r's n_r x p row block, column-major with lda = n_r (n_r from
+ * forge_shard_range(n, r, G)), x[r] the full length-p x, z_blocks[r] its n_r
+ * outputs.  No collective. */
+int forge_sharded_vecmat(forge_group* g, forge_op op, const void* const* A_blocks, uint64_t n,
+                         uint64_t p_cols, const void* const* x, void* const* z_blocks, void* const* ws,
+                         const uint64_t* ws_bytes);
+
 #ifdef __cplusplus
 }
 #endif

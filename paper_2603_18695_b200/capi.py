@@ -145,6 +145,22 @@ _SIGNATURES = {
     "forge_dev_fold": (C.c_int, [C.c_int, _P, _u32, _i32, _P, _P, _P]),
     "forge_dev_copy": (C.c_int, [_P, _P, _u64, _P]),
     "forge_dev_fill_synthetic": (C.c_int, [C.c_int, _P, _u64, _u64, _u64, _i32, _P]),
+    # single-process multi-GPU groups (group.cu)
+    "forge_shard_range": (C.c_int, [_u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_u64)]),
+    "forge_group_create": (C.c_int, [C.POINTER(_i32), _i32, C.POINTER(_P)]),
+    "forge_group_destroy": (C.c_int, [_P]),
+    "forge_group_size": (C.c_int, [_P, C.POINTER(_i32), C.POINTER(_i32)]),
+    "forge_group_stream": (C.c_int, [_P, _i32, C.POINTER(_P)]),
+    "forge_group_synchronize": (C.c_int, [_P]),
+    "forge_sharded_mapreduce": (C.c_int, [_P, C.c_int, C.POINTER(_P), C.POINTER(_u64), C.POINTER(_P),
+                                          C.POINTER(_u64), _P]),
+    "forge_sharded_result_dev": (C.c_int, [_P, _i32, C.POINTER(_P)]),
+    "forge_sharded_scan": (C.c_int, [_P, C.c_int, _i32, C.POINTER(_P), C.POINTER(_P), C.POINTER(_u64),
+                                     C.POINTER(_P), C.POINTER(_u64)]),
+    "forge_sharded_matvec": (C.c_int, [_P, C.c_int, C.POINTER(_P), _u64, _u64, C.POINTER(_P), C.POINTER(_P),
+                                       C.POINTER(_P), C.POINTER(_u64)]),
+    "forge_sharded_vecmat": (C.c_int, [_P, C.c_int, C.POINTER(_P), _u64, _u64, C.POINTER(_P), C.POINTER(_P),
+                                       C.POINTER(_P), C.POINTER(_u64)]),
 }
 
 _lib: C.CDLL | None = None

@@ -114,3 +114,23 @@ def test_no_device_fails_loudly():
     ws = C.c_uint64()
     rc = lib.forge_dev_workspace_bytes(capi.PRIM_SCAN, capi.F32_SUM, 1000, 0, C.byref(ws))
     assert rc == 0 and ws.value > 256   # pure host arithmetic works
+
+
+def test_shard_ranges_and_group_without_device():
+    # forge_shard_range is host arithmetic (shard r = [total*r/G, total*(r+1)/G))
+    from paper_2603_18695_b200 import group
+    for total in (0, 1, 3, 10, 1 << 33, (1 << 64) - 1):
+        for G in (1, 2, 3, 8):
+            spans = [group.shard_range(total, r, G) for r in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(G - 1))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    with pytest.raises(F.ForgeError):
+        group.shard_range(10, 3, 3)
+    lib = capi.load()
+    n = C.c_int()
+    lib.forge_device_count(C.byref(n))
+    if n.value == 0:  # this container: no device, no fallback
+        h = C.c_void_p()
+        devs = (C.c_int32 * 2)(0, 0)
+        assert lib.forge_group_create(devs, 2, C.byref(h)) == capi.ERR_NO_DEVICE

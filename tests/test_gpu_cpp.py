@@ -33,6 +33,18 @@ def test_cpp_composite_shuffle_spec7():
     assert r.stdout.strip().splitlines()[-1].startswith("PASS")
 
 
+@pytest.mark.gpu
+def test_c_group_sharding():
+    # include/forge.h's multi-GPU layer from plain C (gcc, no torch): G = 1
+    # NCCL clique and a G = 3 emulated group, mapreduce + scan vs host folds
+    b = BIN.parent / "test_group"
+    assert b.exists(), "tests/cpp/test_group not built (run __graft_entry__.build())"
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().splitlines()[-1].startswith("PASS")
+
+
 def test_cpp_templates_source_present():
     # CPU-side: the test program exists and exercises every template primitive.
     src = (BIN.parent / "test_templates.cu").read_text()
