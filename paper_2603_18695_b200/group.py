@@ -68,7 +68,7 @@ class Group:
                 if prim == capi.PRIM_SCAN:  # the sharded scan also reduces its shard with this workspace
                     self.ws[r].ensure(dev.workspace_bytes(capi.PRIM_MAPREDUCE, op, ns[r]), self.streams[r])
                 p, b = self.ws[r].for_(prim, op, ns[r], ps[r] if ps else 0, stream=self.streams[r])
-            ptrs.append(p.value)
+            ptrs.append(p)
             sizes.append(b)
         return _ptrs(ptrs), (C.c_uint64 * self.size)(*sizes)
 

@@ -84,7 +84,39 @@ def test_scan_sharded_emulation_carry_in():
         cin = carry if int(has.item()) else None
         dev.scan(op, False, x.data_ptr() + lo * sz, out.data_ptr() + lo * sz, hi - lo, ws, carry_in=cin)
     torch.cuda.synchronize()
+    # against the streaming oracle (exact op: bit for bit), then the single-pass scan
+    bad, _ = orc.check_scan_synthetic(op, False, n, 77, to_np(out, F.s_dtype(op)), 0.0)
+    assert bad == 0, f"{bad} elements of the G-shard scan differ from the oracle"
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("op", [capi.F32_SUM, capi.MAT2_U32])
+def test_native_group_c5_emulated(op):
+    # BASELINE C5's sharded exclusive scan + mapreduce through the native group
+    # layer (forge_sharded_*), G = 4 emulated shards on one GPU, shards generated
+    # in place (index_base = shard start), checked by the streaming oracle.
+    from paper_2603_18695_b200 import group
+    n = (1 << 28) if op == capi.F32_SUM else (1 << 26)
+    seed, G = 0x5EED0C05, 4
+    sz, ss = F.t_dtype(op).itemsize, F.s_dtype(op).itemsize
+    with group.Group([0] * G) as g:
+        src, dst, ns = [], [], []
+        for r in range(G):
+            lo, hi = group.shard_range(n, r, G)
+            t = torch.empty((hi - lo) * sz, dtype=torch.uint8, device="cuda")
+            dev.fill_synthetic(op, t, hi - lo, seed, index_base=lo)
+            src.append(t)
+            dst.append(torch.empty((hi - lo) * ss, dtype=torch.uint8, device="cuda"))
+            ns.append(hi - lo)
+        g.scan(op, False, src, dst, ns)
+        got = np.concatenate([d.cpu().numpy() for d in dst]).view(F.s_dtype(op))
+        bad, worst = orc.check_scan_synthetic(op, False, n, seed, got, TOL.get(op, 0.0))
+        assert bad == 0, f"{bad} mismatches, worst {worst:.3e}"
+        if op == capi.F32_SUM:
+            total = np.frombuffer(g.mapreduce(op, src, ns), dtype=np.float32)
+            want, ex, sc = orc.mapreduce_synthetic(op, n, seed)
+            ok, rel = orc.within(op, total, ex, sc, TOL[op])
+            assert ok, rel
 
 
 @pytest.mark.parametrize("which", ["matvec", "vecmat"])
