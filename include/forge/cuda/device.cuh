@@ -455,12 +455,19 @@ inline const DeviceProps& device_props() {
 // as tickets.  Each launch therefore claims `ws` for its layout `tag`; when
 // the pointer was last used with another tag (or is unknown), the first
 // `zero_bytes` bytes are zeroed on `stream` before the kernel (the reference
-// zero-fills its flags on every launch, primitives.hpp:374, :464-466, :759).
-cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t stream);
+// zero-fills its flags on every launch, primitives.hpp:374, :464-466, :759);
+// with the same tag, only bytes beyond the extent zeroed before.  A claim
+// also invalidates every other claim whose bytes it overlaps (a sub-workspace
+// at an offset, e.g. the lagged scan's tail launch), so those re-zero on
+// their next use.
+// `extent_bytes` (>= zero_bytes; 0 = zero_bytes): every byte of ws the launch
+// may write, for the overlap invalidation.
+cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t stream, uint64_t extent_bytes = 0);
 
 // Layout tags.
 constexpr uint64_t kWsTagTicket = 1;  // mapreduce / ordered reduce: ticket word at offset 0
 constexpr uint64_t kWsTagScan = 2;    // scan: control block + epoch-tagged tile states
+constexpr uint64_t kWsTagScanLag = 3; // lagged scan: control block + tile aggregates + group states
 inline uint64_t ws_tag(uint64_t kind, uint64_t a, uint64_t b = 0) { return kind | (a << 8) | (b << 40); }
 
 __host__ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }

@@ -553,7 +553,10 @@ cudaError_t launch_gevm(const T* A, uint64_t n, uint64_t p, const T* x, S* y, co
     a.tickets = reinterpret_cast<uint32_t*>(w);
     const uint64_t tbytes = round_up(p * sizeof(uint32_t), 256);
     a.partials = reinterpret_cast<S*>(w + tbytes);
-    if (const cudaError_t e = ws_claim(ws, ws_tag(3, tbytes), 256 + tbytes, stream); e != cudaSuccess) return e;
+    if (const cudaError_t e = ws_claim(ws, ws_tag(3, tbytes), 256 + tbytes, stream,
+                                       256 + tbytes + uint64_t(pl.ks) * p * sizeof(S));
+        e != cudaSuccess)
+      return e;
   }
   if constexpr (!Ordered) {
     if (cols) {
@@ -581,7 +584,9 @@ cudaError_t launch_gemv(const T* A, uint64_t n, uint64_t p, const T* x, S* z, co
     char* w = static_cast<char*>(ws) + 256;
     a.tickets = reinterpret_cast<uint32_t*>(w);
     const uint64_t tbytes = round_up(uint64_t(pl.row_blocks) * (pl.groups + 1) * sizeof(uint32_t), 256);
-    if (const cudaError_t e = ws_claim(ws, ws_tag(4, pl.row_blocks, pl.groups), 256 + tbytes, stream);
+    const uint64_t extent = 256 + tbytes + round_up(uint64_t(pl.ks) * n * sizeof(S), 256) +
+                            (pl.groups > 1 ? uint64_t(pl.groups) * n * sizeof(S) : 0);
+    if (const cudaError_t e = ws_claim(ws, ws_tag(4, pl.row_blocks, pl.groups), 256 + tbytes, stream, extent);
         e != cudaSuccess)
       return e;
     w += tbytes;

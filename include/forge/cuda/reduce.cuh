@@ -473,7 +473,9 @@ cudaError_t launch_code_sum(const uint8_t* src, uint64_t n, double off, double s
   // 64-bit partials span the partial and flag areas (>= 8 bytes per block)
   static_assert(sizeof(S) >= 4, "code sums carve 8 bytes per block from S partials + flags");
   auto* parts = reinterpret_cast<unsigned long long*>(parts_s);
-  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream); e != cudaSuccess) return e;
+  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream, MapReduceWs<S>::bytes(mapreduce_max_grid()));
+      e != cudaSuccess)
+    return e;
   code_sum_kernel<S><<<grid, kReduceThreads, 0, stream>>>(src, n, off, scale, parts, ticket, out_dev, out_has_dev);
   return cudaGetLastError();
 }
@@ -490,7 +492,9 @@ cudaError_t launch_mapreduce(const T* src, uint64_t n, uint64_t stride, const F&
   const uint32_t grid = mapreduce_grid<T>(stride == 1 ? n : n * 4);
   MapReduceArgs<T, S, F, Op> a{src, n, stride, f, op, nullptr, nullptr, nullptr, out_dev, out_has_dev};
   MapReduceWs<S>::carve(ws, mapreduce_max_grid(), a.ticket, a.partials, a.part_has);
-  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream); e != cudaSuccess) return e;
+  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream, MapReduceWs<S>::bytes(mapreduce_max_grid()));
+      e != cudaSuccess)
+    return e;
   mapreduce_kernel<T, S, F, Op, mr_unroll<T>()><<<grid, kReduceThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }
@@ -671,7 +675,9 @@ cudaError_t launch_reduce_ordered(const T* src, uint64_t n, uint64_t stride, con
   grid = ntiles ? ceil_div(ntiles, per) : 1;
   OrderedReduceArgs<T, S, F, Op, C> a{src, n, stride, f, op, per, nullptr, nullptr, nullptr, out_dev, out_has_dev};
   OrderedReduceWs<S, Op>::carve(ws, cap, a.ticket, a.partials, a.part_has);
-  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream); e != cudaSuccess) return e;
+  if (const cudaError_t e = ws_claim(ws, kWsTagTicket, 256, stream, OrderedReduceWs<S, Op>::bytes(cap));
+      e != cudaSuccess)
+    return e;
   reduce_ordered_kernel<T, S, F, Op><<<uint32_t(grid), kReduceThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }

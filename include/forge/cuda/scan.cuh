@@ -690,6 +690,347 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
 
 
 // ---------------------------------------------------------------------------
+// Lagged scan: the look-back moved off the tile's critical path.
+//
+// Ticket k does two things with ONE 32 KB shared-memory tile buffer:
+//   A(k)      TMA-load tile k from HBM (L2 evict_last: it is read again soon),
+//             fold it to its aggregate, publish the aggregate (tile state,
+//             written once).  The A of the last tile of a 32-tile GROUP also
+//             folds the group's 32 aggregates and publishes the group
+//             aggregate (group state kind PARTIAL).
+//   B(k - D)  the scan of tile j = k - D, D tiles behind: re-load it (an L2 hit:
+//             D tiles of reads + writes stay well inside the 126 MB L2), fold
+//             its rows, compose with the tile's exclusive prefix, emit, TMA
+//             store; the last tile of a group publishes the group's inclusive
+//             prefix (group state kind PREFIX).
+// j's exclusive prefix needs only states published by LOWER tickets' A phases
+// (tile aggregates of j's group, group aggregates) plus, as a shortcut, group
+// PREFIXes of finished B phases: warp 0 reads them — one 32-lane round of
+// tile aggregates and one of group states, issued together — WHILE A's HBM
+// load is in flight, so the look-back round trips (2-3 us under load,
+// tools/probe_rtt.cu) overlap the load instead of extending the tile's life.
+// Every wait is on a lower ticket's A phase, which waits on nothing but lower
+// tickets: deadlock-free under ticket order like the single-pass kernel.
+//
+// Full tiles only; a partial last tile is scanned by a second (tail) launch
+// seeded with the full tiles' total.
+constexpr uint32_t kLagGroup = 32;  // tiles per group
+
+template <class T, class S, class F, class Op>
+struct LagArgs {
+  ScanArgs<T, S, F, Op> s;  // src, dst, f, op, identity, carry_in, total_out, ctrl, ntiles (full tiles)
+  uint64_t* tagg;           // tile aggregates: STRIDE words per tile, compact
+  uint64_t* gstate;         // group states: STRIDE words per group, compact
+  uint32_t lag;             // D
+  uint32_t nclaims;         // ntiles + D
+};
+
+template <class T, class S, class F, class Op, bool Inclusive>
+__global__ void __launch_bounds__(kScanThreads, 6)
+    scan_lag_kernel(const LagArgs<T, S, F, Op> L, const __grid_constant__ CUtensorMap tmap,
+                    const __grid_constant__ CUtensorMap tmap_out) {
+  using M = ScanMath<S, Op>;
+  using A = typename M::A;
+  using C = typename M::C;
+  using IO = TileStateIO<C>;
+  constexpr int ST = IO::STRIDE;
+  constexpr int IT = smem_scan_items<T>();
+  constexpr int EPC = 16 / int(sizeof(T));
+  constexpr int NCH = kRowBytes / 16;
+  constexpr int NW = kScanThreads / kWarp;
+  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
+  const auto& a = L.s;
+  extern __shared__ unsigned char dyn_smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t s_k, s_epoch, s_phase;
+  __shared__ Opt<A> s_warp[NW];
+  __shared__ Opt<C> s_carry;
+  __shared__ C s_carry_agg;  // A's tile aggregate
+  auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
+  auto cop = [&](const C& x, const C& y) { return M::CT::op(a.op, x, y); };
+  unsigned char* buf =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
+  const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
+
+  // ---- claim; the A load is issued speculatively for blockIdx.x first
+  if (threadIdx.x == 0) {
+    const uint32_t g = blockIdx.x;
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint64_t pol = l2_policy_evict_last();
+    if (g < a.ntiles) {
+      mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+      tma_load_2d_hint(buf, &tmap, 0, int(g) * kScanThreads, &bar, pol);
+    }
+    uint64_t* word = reinterpret_cast<uint64_t*>(a.ctrl);
+    const uint64_t got = atom_add_acq_rel_gpu(word, uint64_t(1));
+    const uint32_t k = uint32_t(got);
+    const uint32_t e = uint32_t(got >> 32);
+    if (k == L.nclaims - 1) st_relaxed_gpu(word, uint64_t(e + 1u) << 32);
+    s_k = k;
+    s_epoch = e;
+    uint32_t ph = 0;  // parity of the barrier's next completion
+    if (k != g) {
+      if (g < a.ntiles) {
+        mbar_wait(&bar, 0);  // drain the speculative copy
+        ph = 1;
+      }
+      if (k < a.ntiles) {
+        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+        tma_load_2d_hint(buf, &tmap, 0, int(k) * kScanThreads, &bar, pol);
+      }
+    }
+    s_phase = ph;
+  }
+  __syncthreads();
+  const uint32_t k = s_k, epoch = s_epoch;
+  uint32_t phase = s_phase;
+  const bool hasA = k < a.ntiles;
+  const bool hasB = k >= L.lag && k - L.lag < a.ntiles;
+  const uint64_t j = uint64_t(k) - L.lag;  // B's tile
+
+  // ---- warp 0: B's exclusive prefix, while A's tile is in flight
+  if (hasB && warp == 0) {
+    const uint64_t grp = j / kLagGroup;
+    const uint32_t r = uint32_t(j % kLagGroup);
+    Opt<C> carry{C{}, false};
+    // in-group: aggregates of tiles grp*32 .. j-1 (lane l: tile grp*32 + l)
+    Opt<C> ing{C{}, false};
+    {
+      C v{};
+      bool ok = lane >= r;
+      while (true) {
+        if (!ok) {
+          uint64_t raw[ST];
+          const uint64_t* p = L.tagg + (grp * kLagGroup + lane) * ST;
+#pragma unroll
+          for (int i = 0; i < ST; i += 2) {
+            if constexpr (ST == 1) raw[0] = ld_relaxed_gpu(p);
+            else ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
+          }
+          ok = IO::decode(raw, epoch, v, a.epoch_mask) != 0;
+        }
+        if (__all_sync(kFullMask, ok)) break;
+      }
+      Opt<C> x{v, lane < r};
+      // ordered fold of lanes 0..r-1 (lane order = tile order)
+#pragma unroll
+      for (unsigned d = 1; d < kWarp; d <<= 1) {
+        Opt<C> got{shfl_down(x.v, d), __shfl_down_sync(kFullMask, int(x.has), d) != 0};
+        if (lane + d < kWarp) x = opt_combine(cop, x, got);
+      }
+      ing = shfl_idx_opt(x, 0);
+    }
+    // group level: states of groups grp-1, grp-2, ... (lane l: group top - l)
+    int64_t top = int64_t(grp) - 1;
+    Opt<C> grp_carry{C{}, false};
+    bool reached_start = top < 0;
+    while (top >= 0) {
+      const int64_t gi = top - int64_t(lane);
+      uint32_t kind = gi < 0 ? 4u : 0u;
+      C v{};
+      while (true) {
+        if (kind == 0) {
+          uint64_t raw[ST];
+          const uint64_t* p = L.gstate + uint64_t(gi) * ST;
+#pragma unroll
+          for (int i = 0; i < ST; i += 2) {
+            if constexpr (ST == 1) raw[0] = ld_relaxed_gpu(p);
+            else ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
+          }
+          kind = IO::decode(raw, epoch, v, a.epoch_mask);
+        }
+        if (__all_sync(kFullMask, kind != 0)) break;
+      }
+      const unsigned pm = __ballot_sync(kFullMask, kind == kPrefix);
+      const int near = pm ? __ffs(int(pm)) - 1 : kWarp;
+      Opt<C> x{v, int(lane) <= near && kind != 4u};
+#pragma unroll
+      for (unsigned d = 1; d < kWarp; d <<= 1) {  // older (higher lane) on the left
+        Opt<C> got{shfl_down(x.v, d), __shfl_down_sync(kFullMask, int(x.has), d) != 0};
+        if (lane + d < kWarp) x = opt_combine(cop, got, x);
+      }
+      grp_carry = opt_combine(cop, shfl_idx_opt(x, 0), grp_carry);
+      if (near < kWarp) break;
+      if (top < int64_t(kWarp)) {
+        reached_start = true;
+        break;
+      }
+      top -= kWarp;
+    }
+    if (reached_start && a.carry_in) carry = Opt<C>{M::CT::to_c(*a.carry_in), true};
+    carry = opt_combine(cop, carry, grp_carry);
+    carry = opt_combine(cop, carry, ing);
+    if (lane == 0) s_carry = carry;
+  }
+
+  // ---- A: fold tile k, publish its aggregate
+  if (hasA) {
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    Opt<A> tot;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const uint4 v = lds128(buf + swz128(threadIdx.x, c));
+      T x[EPC];
+      memcpy(x, &v, 16);
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+        const A y = M::lift(a.f(x[e]));
+        tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
+      }
+    }
+    tot.has = true;
+    tot = warp_scan_incl(aop, tot);
+    if (lane == kWarp - 1) s_warp[warp] = tot;
+    __syncthreads();
+    // the tile aggregate by the SAME tree as B's block scan below (warp scan of
+    // the warp totals), so A's published aggregate and the aggregate B folds
+    // into its group PREFIX are the same bits: the carry a tile gets does not
+    // depend on which of the two the look-back found
+    if (warp == 0) {
+      Opt<A> w = lane < NW ? s_warp[lane] : Opt<A>{A{}, false};
+      w = warp_scan_incl(aop, w);
+      if (lane == NW - 1) {
+        s_carry_agg = M::to_c(w.v);
+        if (a.perturb_ns && ((uint64_t(k) * 0x9E3779B97F4A7C15ull) ^ a.perturb_seed) % 8 == 0) {  // test hook
+          const uint64_t t0 = global_ns();
+          while (global_ns() - t0 < a.perturb_ns) __nanosleep(200);
+        }
+        IO::write(L.tagg, k, IO::GW, epoch, kPartial, M::to_c(w.v));  // compact: tile k at k * ST words
+      }
+    }
+    __syncthreads();
+    // the last tile of a group publishes the group aggregate (warp 1: it polls
+    // the group's other 31 aggregates, published by lower tickets)
+    if (k % kLagGroup == kLagGroup - 1 && warp == 1) {
+      const uint64_t grp = k / kLagGroup;
+      C v{};
+      bool ok = lane == kWarp - 1;
+      if (ok) v = s_carry_agg;  // this tile's own aggregate
+      while (true) {
+        if (!ok) {
+          uint64_t raw[ST];
+          const uint64_t* p = L.tagg + (grp * kLagGroup + lane) * ST;
+#pragma unroll
+          for (int i = 0; i < ST; i += 2) {
+            if constexpr (ST == 1) raw[0] = ld_relaxed_gpu(p);
+            else ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
+          }
+          ok = IO::decode(raw, epoch, v, a.epoch_mask) != 0;
+        }
+        if (__all_sync(kFullMask, ok)) break;
+      }
+      Opt<C> x{v, true};
+#pragma unroll
+      for (unsigned d = 1; d < kWarp; d <<= 1) {
+        Opt<C> got{shfl_down(x.v, d), __shfl_down_sync(kFullMask, int(x.has), d) != 0};
+        if (lane + d < kWarp) x = opt_combine(cop, x, got);
+      }
+      if (lane == 0) IO::write(L.gstate, grp, IO::GW, epoch, kPartial, x.v);
+    }
+  }
+  if (!hasB) return;
+
+  // ---- B: re-load tile j (L2), scan it with the carry, store
+  __syncthreads();  // every read of A's tile is done (and s_carry is visible)
+  if (threadIdx.x == 0) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+    tma_load_2d_hint(buf, &tmap, 0, int(j) * kScanThreads, &bar, l2_policy_evict_first());
+  }
+  mbar_wait(&bar, phase);
+  Opt<A> tot;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const uint4 v = lds128(buf + swz128(threadIdx.x, c));
+    T x[EPC];
+    memcpy(x, &v, 16);
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) {
+      const A y = M::lift(a.f(x[e]));
+      tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
+    }
+  }
+  tot.has = true;
+  Opt<A> incl = warp_scan_incl(aop, tot);
+  __syncthreads();  // s_warp reuse: A's readers are done
+  if (lane == kWarp - 1) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    Opt<A> w = lane < NW ? s_warp[lane] : Opt<A>{A{}, false};
+    w = warp_scan_incl(aop, w);
+    if (lane < NW) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const Opt<C> carry = s_carry;
+  if (threadIdx.x == 0 && (j % kLagGroup == kLagGroup - 1 || j == a.ntiles - 1)) {
+    const C pre = carry.has ? cop(carry.v, M::to_c(s_warp[NW - 1].v)) : M::to_c(s_warp[NW - 1].v);
+    if (j % kLagGroup == kLagGroup - 1) IO::write(L.gstate, j / kLagGroup, IO::GW, epoch, kPrefix, pre);
+    if (j == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
+  }
+  Opt<A> run;
+  {
+    const Opt<A> warp_ex = warp > 0 ? s_warp[warp - 1] : Opt<A>{A{}, false};
+    Opt<A> lane_ex = shfl_up_opt(incl, 1);
+    if (lane == 0) lane_ex.has = false;
+    const Opt<A> tile_ex = carry.has ? Opt<A>{M::from_c(carry.v), true} : Opt<A>{A{}, false};
+    run = opt_combine(aop, opt_combine(aop, tile_ex, warp_ex), lane_ex);
+  }
+  using E = std::conditional_t<M::kNarrowEmit, S, A>;
+  Opt<E> em;
+  if constexpr (M::kNarrowEmit)
+    em = Opt<E>{M::lower(run.v), run.has};
+  else
+    em = run;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const uint4 v = lds128(buf + swz128(threadIdx.x, c));
+    T x[EPC];
+    memcpy(x, &v, 16);
+    S o[EPC];
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) {
+      E y;
+      if constexpr (M::kNarrowEmit) y = a.f(x[e]);
+      else y = M::lift(a.f(x[e]));
+      auto eop = [&](const E& p, const E& q) {
+        if constexpr (M::kNarrowEmit) return a.op(p, q);
+        else return aop(p, q);
+      };
+      auto elower = [&](const E& w) {
+        if constexpr (M::kNarrowEmit) return w;
+        else return M::lower(w);
+      };
+      if constexpr (Inclusive) {
+        em.v = em.has ? eop(em.v, y) : y;
+        em.has = true;
+        o[e] = elower(em.v);
+      } else {
+        o[e] = em.has ? elower(em.v) : a.identity;
+        em.v = em.has ? eop(em.v, y) : y;
+        em.has = true;
+      }
+    }
+    if constexpr (sizeof(S) == sizeof(T)) {
+      uint4 w;
+      memcpy(&w, o, 16);
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(buf + swz128(threadIdx.x, c))), "r"(w.x),
+                   "r"(w.y), "r"(w.z), "r"(w.w)
+                   : "memory");
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_2d_hint(&tmap_out, 0, int(j) * kScanThreads, buf, l2_policy_evict_first());
+    tma_store_commit();
+    tma_store_wait_read();
+  }
+}
+
+
+// ---------------------------------------------------------------------------
 // Workspace + launch.
 
 // Workspace: [256-byte control block (ticket, epoch) | one slot per group of
@@ -726,6 +1067,20 @@ struct ScanWs {
   static uint64_t claim_bytes(uint64_t tiles, uint32_t stride) { return 256 + IO::slots(tiles) * stride * 8; }
 };
 
+template <class T, class S, class Op>
+struct LagWs {
+  using C = typename CarryTraits<S, Op>::C;
+  static constexpr uint64_t ST = uint64_t(TileStateIO<C>::STRIDE);
+  static constexpr uint64_t align(uint64_t v) { return (v + 255) & ~uint64_t(255); }
+  static uint64_t tagg_off() { return 256; }
+  static uint64_t gstate_off(uint64_t tiles) { return tagg_off() + align(tiles * ST * 8); }
+  static uint64_t total_off(uint64_t tiles) { return gstate_off(tiles) + align(ceil_div(tiles, kLagGroup) * ST * 8); }
+  static uint64_t tail_off(uint64_t tiles) { return total_off(tiles) + 256; }
+  static uint64_t bytes(uint64_t tiles, uint64_t tile_items) {
+    return tail_off(tiles) + ScanWs<T, S, Op>::bytes(tile_items);
+  }
+};
+
 // Development knobs (FORGE_DEV builds only; constants otherwise).
 inline uint32_t scan_lookback_mode() {
   static const uint32_t v = dev_knob("FORGE_SCAN_LOOKBACK", 0);
@@ -737,6 +1092,16 @@ inline uint32_t scan_backoff_ns() {
 }
 inline bool scan_force_regs() {
   static const bool v = dev_knob("FORGE_SCAN_REGS", 0) != 0;
+  return v;
+}
+// Lag D of the lagged scan (scan_lag_kernel), in tiles; 0 = the single-pass
+// kernel.  Measured on B200 (148 SMs, f32 / i32 / affine / argmax at 2^28,
+// GB/s): D = 256: 4133 / 3744 / 3757 / 3401 (B waits for A's aggregates);
+// 448: 5368 / 5287 / 5038 / 4617; 512: 5290 / 5290 / 5112 / 4637; 768: 5184 /
+// 5185 / 4852 / 4427 (the re-read starts missing L2); single-pass kernel:
+// 4828 / 4849 / 4479 / 4517.  D scales with the resident tiles: 3.5 per SM.
+inline uint32_t scan_lag() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_LAG", device_props().sm_count * 7 / 2);
   return v;
 }
 inline bool scan_no_tma_store() {
@@ -815,6 +1180,47 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
+  if constexpr (smem_scan_type_ok<T>() && sizeof(S) == sizeof(T) && sizeof(T) < 16) {
+    if (const uint32_t lag = scan_lag(); lag && src_stride == 1 && dst_stride == 1) {
+      constexpr uint64_t kTile = uint64_t(kScanThreads) * smem_scan_items<T>();
+      using LW = LagWs<T, S, Op>;
+      const uint64_t nfull = n / kTile;
+      const uint64_t tail = n - nfull * kTile;
+      CUtensorMap tin, tout;
+      if (nfull >= 4 * kLagGroup && nfull + lag < (1ull << 31) && ws_bytes >= LW::bytes(nfull, kTile) &&
+          make_rows128_map(&tin, src, nfull * kTile * sizeof(T) / kRowBytes, uint32_t(kScanThreads)) &&
+          make_rows128_map(&tout, dst, nfull * kTile * sizeof(S) / kRowBytes, uint32_t(kScanThreads))) {
+        char* w = static_cast<char*>(ws);
+        LagArgs<T, S, F, Op> L{a, reinterpret_cast<uint64_t*>(w + LW::tagg_off()),
+                               reinterpret_cast<uint64_t*>(w + LW::gstate_off(nfull)), lag,
+                               uint32_t(nfull + lag)};
+        L.s.ntiles = uint32_t(nfull);
+        S* full_total = reinterpret_cast<S*>(w + LW::total_off(nfull));
+        L.s.total_out = tail ? full_total : total_out;
+        if (const cudaError_t e = ws_claim(ws, kWsTagScanLag, LW::tail_off(nfull), stream); e != cudaSuccess) return e;
+        auto kern = inclusive ? scan_lag_kernel<T, S, F, Op, true> : scan_lag_kernel<T, S, F, Op, false>;
+        static thread_local int done_dev = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (done_dev != dev) {
+          cudaFuncSetAttribute(scan_lag_kernel<T, S, F, Op, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kSmemScanDyn));
+          cudaFuncSetAttribute(scan_lag_kernel<T, S, F, Op, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kSmemScanDyn));
+          cudaFuncSetAttribute(scan_lag_kernel<T, S, F, Op, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          cudaFuncSetAttribute(scan_lag_kernel<T, S, F, Op, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          done_dev = dev;
+        }
+        kern<<<uint32_t(nfull + lag), kScanThreads, kSmemScanDyn, stream>>>(L, tin, tout);
+        if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess || !tail) return e;
+        // the partial last tile: a tail launch seeded with the full tiles' total
+        const uint64_t off = nfull * kTile;
+        return launch_scan<T, S, F, Op>(src + off, 1, dst + off, 1, tail, inclusive, f, op, identity, full_total,
+                                        total_out, w + LW::tail_off(nfull), ws_bytes - LW::tail_off(nfull), stream,
+                                        hooks);
+      }
+    }
+  }
   if constexpr (smem_scan_type_ok<T>()) {
     constexpr int R = scan_subtiles<T>();
     constexpr uint64_t kTile = uint64_t(R) * kScanThreads * smem_scan_items<T>();

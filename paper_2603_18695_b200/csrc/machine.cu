@@ -11,7 +11,7 @@
 #include <cstdio>
 #include <mutex>
 
-#include <unordered_map>
+#include <map>
 
 #include "forge/cuda/device.cuh"
 #include "forge/machine.hpp"
@@ -20,17 +20,38 @@ namespace forge {
 
 namespace cuda {
 
-cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t stream) {
+cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t stream, uint64_t extent_bytes) {
+  // base address -> {layout tag, bytes zeroed for it, bytes its kernels write}
+  struct Claim {
+    uint64_t tag, zeroed, extent;
+  };
   static std::mutex mu;
-  static std::unordered_map<const void*, uint64_t> last;  // workspace base -> layout tag
+  static std::map<uintptr_t, Claim> reg;
+  const uintptr_t p = reinterpret_cast<uintptr_t>(ws);
+  const uint64_t extent = std::max<uint64_t>({extent_bytes, zero_bytes, 1});
+  uint64_t lo = 0;  // zero [lo, zero_bytes)
   {
     std::lock_guard<std::mutex> g(mu);
-    auto it = last.find(ws);
-    if (it != last.end() && it->second == tag) return cudaSuccess;
-    if (last.size() >= 4096) last.clear();  // forgetting only costs a memset on next use
-    last[ws] = tag;
+    auto it = reg.find(p);
+    if (it != reg.end() && it->second.tag == tag) {
+      lo = std::min(it->second.zeroed, zero_bytes);  // same layout: only bytes not zeroed before
+      it->second.zeroed = std::max(it->second.zeroed, zero_bytes);
+      it->second.extent = std::max(it->second.extent, extent);
+    } else {
+      if (it != reg.end()) reg.erase(it);
+      reg[p] = Claim{tag, zero_bytes, extent};
+    }
+    // every other claim overlapping [p, p + extent) lost its bytes to this
+    // layout: nested ones, and one below p whose extent reaches into it
+    reg.erase(reg.upper_bound(p), reg.lower_bound(p + extent));
+    auto at = reg.find(p);
+    if (at != reg.begin()) {
+      auto below = std::prev(at);
+      if (below->first + below->second.extent > p) reg.erase(below);
+    }
+    if (reg.size() >= 4096) reg.clear();  // forgetting only costs a memset on next use
   }
-  return zero_bytes ? cudaMemsetAsync(ws, 0, zero_bytes, stream) : cudaSuccess;
+  return zero_bytes > lo ? cudaMemsetAsync(static_cast<char*>(ws) + lo, 0, zero_bytes - lo, stream) : cudaSuccess;
 }
 
 }  // namespace cuda
