@@ -418,6 +418,25 @@ int forge_sharded_vecmat(forge_group* g, forge_op op, const void* const* A_block
                          uint64_t p_cols, const void* const* x, void* const* z_blocks, void* const* ws,
                          const uint64_t* ws_bytes);
 
+/* scan over BLOCK-CYCLIC shards with a cross-GPU decoupled look-back
+ * (the protocol of prim::scan, primitives.hpp:518-576,
+ * extended across devices): the global array of n elements is cut into chunks
+ * of chunk_elems (a positive multiple of forge_cyclic_chunk_quantum(op));
+ * chunk c lives on shard c mod G, each shard holding its chunks back to back
+ * (forge_cyclic_local_n elements).  Tile states live on their owner and are
+ * read by the next shard over peer memory (NVLink / NVSwitch; peer access is
+ * enabled on first use): no collective, 2n/G HBM bytes per GPU (reduce-then-
+ * scan: 3n/G).  dst[r] receives shard r's elements of the global scan, same
+ * layout.  ws_bytes[r] >= forge_cyclic_workspace_bytes(op, local_n).  Ops with
+ * sizeof(S) == sizeof(T) <= 8 bytes; an emulated group needs
+ * (chunk_elems / quantum) * G <= the SM count (one launch serves all shards). */
+int forge_cyclic_chunk_quantum(forge_op op, uint64_t* elems);
+int forge_cyclic_local_n(uint64_t n, uint64_t chunk_elems, int32_t rank, int32_t count, uint64_t* local_n);
+int forge_cyclic_workspace_bytes(forge_op op, uint64_t local_n, uint64_t* bytes);
+int forge_sharded_scan_cyclic(forge_group* g, forge_op op, int32_t inclusive, const void* const* src,
+                              void* const* dst, uint64_t n, uint64_t chunk_elems, void* const* ws,
+                              const uint64_t* ws_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -468,6 +468,7 @@ cudaError_t ws_claim(void* ws, uint64_t tag, uint64_t zero_bytes, cudaStream_t s
 constexpr uint64_t kWsTagTicket = 1;  // mapreduce / ordered reduce: ticket word at offset 0
 constexpr uint64_t kWsTagScan = 2;    // scan: control block + epoch-tagged tile states
 constexpr uint64_t kWsTagScanLag = 3; // lagged scan: control block + tile aggregates + group states
+constexpr uint64_t kWsTagScanCyclic = 4;  // cross-GPU cyclic scan: ticket + per-local-tile states
 inline uint64_t ws_tag(uint64_t kind, uint64_t a, uint64_t b = 0) { return kind | (a << 8) | (b << 40); }
 
 __host__ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }

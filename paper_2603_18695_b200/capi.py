@@ -161,6 +161,11 @@ _SIGNATURES = {
                                        C.POINTER(_P), C.POINTER(_u64)]),
     "forge_sharded_vecmat": (C.c_int, [_P, C.c_int, C.POINTER(_P), _u64, _u64, C.POINTER(_P), C.POINTER(_P),
                                        C.POINTER(_P), C.POINTER(_u64)]),
+    "forge_cyclic_chunk_quantum": (C.c_int, [C.c_int, C.POINTER(_u64)]),
+    "forge_cyclic_local_n": (C.c_int, [_u64, _u64, _i32, _i32, C.POINTER(_u64)]),
+    "forge_cyclic_workspace_bytes": (C.c_int, [C.c_int, _u64, C.POINTER(_u64)]),
+    "forge_sharded_scan_cyclic": (C.c_int, [_P, C.c_int, _i32, C.POINTER(_P), C.POINTER(_P), _u64, _u64,
+                                            C.POINTER(_P), C.POINTER(_u64)]),
 }
 
 _lib: C.CDLL | None = None

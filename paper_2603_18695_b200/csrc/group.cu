@@ -20,14 +20,18 @@
 //              n x p_r column block (contiguous in column-major), x replicated.
 //   vecmat     (gemv, :795-807) rows sharded: shard r holds the n_r x p row
 //              block (column-major, lda = n_r), x replicated.  No collective.
+//   scan_cyclic  block-cyclic chunks with a cross-GPU decoupled look-back over
+//              peer memory (forge/cuda/scan_cyclic.cuh): 2n/G bytes per GPU.
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <vector>
 
 #include "capi_common.cuh"
+#include "forge/cuda/scan_cyclic.cuh"
 
 using namespace forge::capi;
 
@@ -418,6 +422,171 @@ int forge_sharded_vecmat(forge_group* g, forge_op op, const void* const* A_block
         return rc;
     }
     return FORGE_OK;
+  });
+}
+
+// ---- cross-GPU decoupled look-back over block-cyclic chunks (scan_cyclic.cuh)
+
+int forge_cyclic_chunk_quantum(forge_op op, uint64_t* elems) {
+  return guarded([&]() -> int {
+    int rc = menu::visit1(op, [&](auto e) -> int {
+      using T = typename decltype(e)::T;
+      using S = typename decltype(e)::S;
+      if constexpr (!cuda::smem_scan_type_ok<T>() || sizeof(S) != sizeof(T) || sizeof(T) > 8) {
+        set_error("Unsupported: the cyclic scan takes ops with sizeof(S) == sizeof(T) <= 8");
+        return FORGE_ERR_UNSUPPORTED;
+      } else {
+        *elems = cuda::cyclic_tile_elems<T>();
+        return FORGE_OK;
+      }
+    });
+    return rc;
+  });
+}
+
+int forge_cyclic_local_n(uint64_t n, uint64_t chunk_elems, int32_t rank, int32_t count, uint64_t* local_n) {
+  return guarded([&]() -> int {
+    if (count <= 0 || rank < 0 || rank >= count || chunk_elems == 0 || !local_n) {
+      set_error("InvalidArgument: forge_cyclic_local_n needs 0 <= rank < count and chunk_elems > 0");
+      return FORGE_ERR_INVALID_ARGUMENT;
+    }
+    *local_n = cuda::cyclic_local_n(n, chunk_elems, uint32_t(rank), uint32_t(count));
+    return FORGE_OK;
+  });
+}
+
+int forge_cyclic_workspace_bytes(forge_op op, uint64_t local_n, uint64_t* bytes) {
+  return guarded([&]() -> int {
+    return menu::visit1(op, [&](auto e) -> int {
+      using E = decltype(e);
+      *bytes = cuda::cyclic_ws_bytes<typename E::T, typename E::S, typename E::Op>(local_n);
+      return FORGE_OK;
+    });
+  });
+}
+
+int forge_sharded_scan_cyclic(forge_group* g, forge_op op, int32_t inclusive, const void* const* src,
+                              void* const* dst, uint64_t n, uint64_t chunk_elems, void* const* ws,
+                              const uint64_t* ws_bytes) {
+  forge::prim::detail::NvtxRange nvtx_range("forge_sharded_scan_cyclic");
+  return guarded([&]() -> int {
+    if (int rc = check_group(g); rc) return rc;
+    const int G = g->size();
+    if (G > cuda::kCyclicMaxShards) {
+      set_error("Unsupported: the cyclic scan takes at most 8 shards");
+      return FORGE_ERR_UNSUPPORTED;
+    }
+    uint64_t quantum = 0;
+    if (int rc = forge_cyclic_chunk_quantum(op, &quantum); rc) return rc;
+    if (chunk_elems == 0 || chunk_elems % quantum) {
+      set_error("InvalidArgument: chunk_elems must be a positive multiple of forge_cyclic_chunk_quantum (" +
+                std::to_string(quantum) + ")");
+      return FORGE_ERR_INVALID_ARGUMENT;
+    }
+    const uint64_t tpc = chunk_elems / quantum;
+    if (tpc >= (1ull << 31) || cuda::ceil_div(n, quantum) >= (1ull << 31)) {
+      set_error("InvalidArgument: too many tiles for the cyclic scan");
+      return FORGE_ERR_INVALID_ARGUMENT;
+    }
+    if (g->emulated && tpc * uint64_t(G) > uint64_t(cuda::device_props().sm_count)) {
+      // one launch deals tickets round-robin to the virtual shards: a tile may
+      // wait on a ticket up to tpc * G ahead, which must be resident
+      set_error("InvalidArgument: an emulated group needs chunk tiles * shards <= SM count (" +
+                std::to_string(cuda::device_props().sm_count) + ")");
+      return FORGE_ERR_INVALID_ARGUMENT;
+    }
+    DeviceGuard guard;
+    if (!g->emulated && G > 1) {  // peer access: every shard reads its predecessor's tile states
+      for (const Shard& a : g->shards) {
+        if (int rc = use(a); rc) return rc;
+        for (const Shard& b : g->shards) {
+          if (a.device == b.device) continue;
+          int ok = 0;
+          cudaDeviceCanAccessPeer(&ok, a.device, b.device);
+          if (!ok) {
+            set_error("Unsupported: no peer access between the group's devices (NVLink / NVSwitch needed)");
+            return FORGE_ERR_UNSUPPORTED;
+          }
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return from_cuda(e, "peer access");
+          cudaGetLastError();
+        }
+      }
+    }
+    static std::atomic<uint32_t> epochs{0};
+    uint32_t epoch = 0;
+    while (epoch == 0) epoch = (epochs.fetch_add(1) + 1) & 0x3fffffffu;  // process-wide, never 0
+    return menu::visit1(op, [&](auto e) -> int {
+      using E = decltype(e);
+      using T = typename E::T;
+      using S = typename E::S;
+      if constexpr (!cuda::smem_scan_type_ok<T>() || sizeof(S) != sizeof(T) || sizeof(T) > 8) {
+        return FORGE_ERR_UNSUPPORTED;
+      } else {
+        cuda::CyclicArgs<T, S, typename E::F, typename E::Op> a{};
+        a.n = n;
+        a.tiles = cuda::ceil_div(n, quantum);
+        a.tpc = uint32_t(tpc);
+        a.G = uint32_t(G);
+        a.epoch = epoch;
+        a.f = typename E::F{};
+        a.op = typename E::Op{};
+        a.identity = e.identity;
+        for (int r = 0; r < G; ++r) {
+          const uint64_t ln = cuda::cyclic_local_n(n, chunk_elems, uint32_t(r), uint32_t(G));
+          const uint64_t need = cuda::cyclic_ws_bytes<T, S, typename E::Op>(ln);
+          if (int w = require_ws(ws_bytes[r], need, "cyclic scan"); w) return w;
+          a.states[r] = reinterpret_cast<uint64_t*>(static_cast<char*>(ws[r]) + 256);
+          const Shard& s = g->shards[r];
+          if (int rc = use(s); rc) return rc;
+          if (int rc = from_cuda(cuda::ws_claim(ws[r], cuda::kWsTagScanCyclic, need, s.stream), "workspace"); rc)
+            return rc;
+        }
+        if (g->emulated || G == 1) {
+          // one launch over all (virtual) shards, on shard 0's stream
+          const Shard& s0 = g->shards[0];
+          if (int rc = use(s0); rc) return rc;
+          std::vector<cudaEvent_t> ev(G);
+          for (int r = 1; r < G; ++r) {
+            cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming);
+            cudaEventRecord(ev[r], g->shards[r].stream);
+            cudaStreamWaitEvent(s0.stream, ev[r], 0);
+          }
+          a.rank0 = 0;
+          a.nvirt = uint32_t(G);
+          a.ctrl = static_cast<uint32_t*>(ws[0]);
+          for (int r = 0; r < G; ++r) {
+            a.src[r] = static_cast<const T*>(src[r]);
+            a.dst[r] = static_cast<S*>(dst[r]);
+            a.local_n[r] = cuda::cyclic_local_n(n, chunk_elems, uint32_t(r), uint32_t(G));
+          }
+          int rc = from_cuda(cuda::launch_scan_cyclic(a, inclusive != 0, s0.stream), "cyclic scan launch");
+          cudaEvent_t done;
+          cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+          cudaEventRecord(done, s0.stream);
+          for (int r = 1; r < G; ++r) {
+            cudaStreamWaitEvent(g->shards[r].stream, done, 0);
+            cudaEventDestroy(ev[r]);
+          }
+          cudaEventDestroy(done);
+          return rc;
+        }
+        for (int r = 0; r < G; ++r) {  // one launch per device, each over its own shard
+          const Shard& s = g->shards[r];
+          if (int rc = use(s); rc) return rc;
+          auto ar = a;
+          ar.rank0 = uint32_t(r);
+          ar.nvirt = 1;
+          ar.ctrl = static_cast<uint32_t*>(ws[r]);
+          ar.src[0] = static_cast<const T*>(src[r]);
+          ar.dst[0] = static_cast<S*>(dst[r]);
+          ar.local_n[0] = cuda::cyclic_local_n(n, chunk_elems, uint32_t(r), uint32_t(G));
+          if (int rc = from_cuda(cuda::launch_scan_cyclic(ar, inclusive != 0, s.stream), "cyclic scan launch"); rc)
+            return rc;
+        }
+        return FORGE_OK;
+      }
+    });
   });
 }
 

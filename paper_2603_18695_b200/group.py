@@ -24,6 +24,26 @@ def shard_range(total: int, rank: int, count: int) -> tuple[int, int]:
     return lo.value, hi.value
 
 
+def cyclic_quantum(op: int) -> int:
+    q = C.c_uint64()
+    check(capi.load().forge_cyclic_chunk_quantum(op, C.byref(q)))
+    return q.value
+
+
+def cyclic_local_n(n: int, chunk: int, rank: int, count: int) -> int:
+    out = C.c_uint64()
+    check(capi.load().forge_cyclic_local_n(n, chunk, rank, count, C.byref(out)))
+    return out.value
+
+
+def cyclic_split(n: int, chunk: int, G: int) -> list[list[tuple[int, int]]]:
+    """Global [lo, hi) ranges of every shard's chunks, in its local order."""
+    out = [[] for _ in range(G)]
+    for c, lo in enumerate(range(0, n, chunk)):
+        out[c % G].append((lo, min(lo + chunk, n)))
+    return out
+
+
 def _ptrs(ts) -> C.Array:
     return (C.c_void_p * len(ts))(*[C.c_void_p(t if isinstance(t, int) else t.data_ptr()) for t in ts])
 
@@ -111,4 +131,23 @@ class Group:
         rows = [shard_range(n, r, self.size) for r in range(self.size)]
         ws, wb = self._workspaces(capi.PRIM_VECMAT, op, [max(hi - lo, 1) for lo, hi in rows], [p] * self.size)
         check(self.lib.forge_sharded_vecmat(self.h, op, _ptrs(A_blocks), n, p, _ptrs(xs), _ptrs(zs), ws, wb))
+        self._leave(sync)
+
+    def scan_cyclic(self, op: int, inclusive: bool, src: list, dst: list, n: int, chunk: int,
+                    sync: bool = True) -> None:
+        """Scan of a block-cyclic array (chunk c on shard c mod G) with the
+        cross-GPU decoupled look-back; src[r] / dst[r] hold shard r's chunks
+        back to back (cyclic_split gives their global ranges)."""
+        self._enter()
+        ptrs, sizes = [], []
+        for r in range(self.size):
+            with torch.cuda.device(self.devices[r]):
+                need = C.c_uint64()
+                check(self.lib.forge_cyclic_workspace_bytes(op, cyclic_local_n(n, chunk, r, self.size),
+                                                            C.byref(need)))
+                b = self.ws[r].ensure(need.value, self.streams[r])
+            ptrs.append(b.data_ptr())
+            sizes.append(b.numel())
+        check(self.lib.forge_sharded_scan_cyclic(self.h, op, 1 if inclusive else 0, _ptrs(src), _ptrs(dst), n, chunk,
+                                                 _ptrs(ptrs), (C.c_uint64 * self.size)(*sizes)))
         self._leave(sync)

@@ -109,3 +109,69 @@ def test_group_errors():
     assert e.value.status == capi.ERR_INVALID_ARGUMENT
     with pytest.raises(F.ForgeError):
         group.Group([0, 99])
+
+
+# ---- block-cyclic shards + cross-GPU decoupled look-back (forge_sharded_scan_cyclic)
+
+@pytest.mark.parametrize("op", [capi.I32_SUM, capi.ARGMAX_F32I32, capi.F32_SUM, capi.AFFINE_F32])
+@pytest.mark.parametrize("inclusive", [True, False])
+def test_group_scan_cyclic(grp, op, inclusive):
+    q = group.cyclic_quantum(op)
+    G = grp.size
+    tpc = max(1, min(16, 148 // G))           # chunk tiles: the emulated group needs tpc * G <= SMs
+    chunk = tpc * q
+    for n in (5, chunk - 3, 3 * chunk + 17, (4 * G + 1) * chunk + q // 2 + 1, 64 * chunk):
+        x = orc.fill(op, n, 0x6D0 + op + n)
+        spans = group.cyclic_split(n, chunk, G)
+        ss = F.s_dtype(op).itemsize
+        src, dst = [], []
+        for r in range(G):
+            local = np.concatenate([x[lo:hi] for lo, hi in spans[r]]) if spans[r] else x[:0]
+            assert len(local) == group.cyclic_local_n(n, chunk, r, G)
+            src.append(dev_bytes(local))
+            dst.append(torch.empty(max(len(local), 1) * ss, dtype=torch.uint8, device="cuda"))
+        grp.scan_cyclic(op, inclusive, src, dst, n, chunk)
+        got = np.empty(n, dtype=F.s_dtype(op))
+        for r in range(G):
+            loc = dst[r].cpu().numpy().view(F.s_dtype(op))
+            off = 0
+            for lo, hi in spans[r]:
+                got[lo:hi] = loc[off: off + hi - lo]
+                off += hi - lo
+        want, ex, sc = orc.scan(op, inclusive, x)
+        assert_match(op, got, want, ex, sc, f"cyclic scan G={G} n={n} chunk={chunk}")
+
+
+def test_group_scan_cyclic_relaunch_bitexact(grp):
+    # the relaunch stress of the single-pass protocol, across shards: one
+    # workspace set, two inputs alternating, every output bit-exact
+    op, G = capi.I32_SUM, grp.size
+    q = group.cyclic_quantum(op)
+    chunk = max(1, min(16, 148 // G)) * q
+    n = 40 * chunk + 1234
+    spans = group.cyclic_split(n, chunk, G)
+    ins, wants = [], []
+    for k in range(2):
+        x = orc.fill(op, n, 0x6E0 + k)
+        ins.append([dev_bytes(np.concatenate([x[lo:hi] for lo, hi in spans[r]])) for r in range(G)])
+        wants.append(orc.scan(op, True, x)[0])
+    dst = [torch.empty(group.cyclic_local_n(n, chunk, r, G) * 4, dtype=torch.uint8, device="cuda") for r in range(G)]
+    for i in range(12):
+        grp.scan_cyclic(op, True, ins[i % 2], dst, n, chunk)
+        got = np.empty(n, dtype=np.int32)
+        for r in range(G):
+            loc = dst[r].cpu().numpy().view(np.int32)
+            off = 0
+            for lo, hi in spans[r]:
+                got[lo:hi] = loc[off: off + hi - lo]
+                off += hi - lo
+        assert np.array_equal(got, wants[i % 2]), i
+
+
+def test_group_scan_cyclic_rejects():
+    with group.Group([0, 0]) as g:
+        x = torch.zeros(64, dtype=torch.uint8, device="cuda")
+        with pytest.raises(F.ForgeError):  # 16-byte elements: single-pass protocol only
+            g.scan_cyclic(capi.MAT2_U32, True, [x, x], [x, x], 2, group.cyclic_quantum(capi.I32_SUM))
+        with pytest.raises(F.ForgeError):  # chunk not a multiple of the tile
+            g.scan_cyclic(capi.I32_SUM, True, [x, x], [x, x], 16, 100)
