@@ -983,43 +983,58 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     em = Opt<E>{M::lower(run.v), run.has};
   else
     em = run;
+  // the running value is present for every row but the global first one:
+  // the per-element has-checks (selects) only run in that row
+  auto emit_rows = [&](auto has_tag) {
+    constexpr bool kHas = decltype(has_tag)::value;
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const uint4 v = lds128(buf + swz128(threadIdx.x, c));
-    T x[EPC];
-    memcpy(x, &v, 16);
-    S o[EPC];
+    for (int c = 0; c < NCH; ++c) {
+      const uint4 v = lds128(buf + swz128(threadIdx.x, c));
+      T x[EPC];
+      memcpy(x, &v, 16);
+      S o[EPC];
 #pragma unroll
-    for (int e = 0; e < EPC; ++e) {
-      E y;
-      if constexpr (M::kNarrowEmit) y = a.f(x[e]);
-      else y = M::lift(a.f(x[e]));
-      auto eop = [&](const E& p, const E& q) {
-        if constexpr (M::kNarrowEmit) return a.op(p, q);
-        else return aop(p, q);
-      };
-      auto elower = [&](const E& w) {
-        if constexpr (M::kNarrowEmit) return w;
-        else return M::lower(w);
-      };
-      if constexpr (Inclusive) {
-        em.v = em.has ? eop(em.v, y) : y;
-        em.has = true;
-        o[e] = elower(em.v);
-      } else {
-        o[e] = em.has ? elower(em.v) : a.identity;
-        em.v = em.has ? eop(em.v, y) : y;
-        em.has = true;
+      for (int e = 0; e < EPC; ++e) {
+        E y;
+        if constexpr (M::kNarrowEmit) y = a.f(x[e]);
+        else y = M::lift(a.f(x[e]));
+        auto eop = [&](const E& p, const E& q) {
+          if constexpr (M::kNarrowEmit) return a.op(p, q);
+          else return aop(p, q);
+        };
+        auto elower = [&](const E& w) {
+          if constexpr (M::kNarrowEmit) return w;
+          else return M::lower(w);
+        };
+        if constexpr (kHas) {
+          if constexpr (Inclusive) {
+            em.v = eop(em.v, y);
+            o[e] = elower(em.v);
+          } else {
+            o[e] = elower(em.v);
+            em.v = eop(em.v, y);
+          }
+        } else if constexpr (Inclusive) {
+          em.v = em.has ? eop(em.v, y) : y;
+          em.has = true;
+          o[e] = elower(em.v);
+        } else {
+          o[e] = em.has ? elower(em.v) : a.identity;
+          em.v = em.has ? eop(em.v, y) : y;
+          em.has = true;
+        }
       }
-    }
-    if constexpr (sizeof(S) == sizeof(T)) {
       uint4 w;
       memcpy(&w, o, 16);
-      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(buf + swz128(threadIdx.x, c))), "r"(w.x),
-                   "r"(w.y), "r"(w.z), "r"(w.w)
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(buf + swz128(threadIdx.x, c))),
+                   "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
                    : "memory");
     }
-  }
+  };
+  if (em.has)
+    emit_rows(std::true_type{});
+  else
+    emit_rows(std::false_type{});
   fence_proxy_async_smem();
   __syncthreads();
   if (threadIdx.x == 0) {
