@@ -1109,6 +1109,9 @@ inline bool scan_force_regs() {
   static const bool v = dev_knob("FORGE_SCAN_REGS", 0) != 0;
   return v;
 }
+#ifndef FORGE_SCAN_LAG_MAX_T
+#define FORGE_SCAN_LAG_MAX_T 16  // largest element (bytes) taken by the lagged scan
+#endif
 // Lag D of the lagged scan (scan_lag_kernel), in tiles; 0 = the single-pass
 // kernel.  Measured on B200 (148 SMs, f32 / i32 / affine / argmax at 2^28,
 // GB/s): D = 256: 4133 / 3744 / 3757 / 3401 (B waits for A's aggregates);
@@ -1195,7 +1198,10 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
-  if constexpr (smem_scan_type_ok<T>() && sizeof(S) == sizeof(T) && sizeof(T) < 16) {
+  // lagged scan: elements and carries of at most 16 bytes (a 32-byte f64
+  // quaternion carry spills at 6 CTAs/SM: 3.20 TB/s lagged vs 3.57 single-pass)
+  if constexpr (smem_scan_type_ok<T>() && sizeof(S) == sizeof(T) && sizeof(T) <= FORGE_SCAN_LAG_MAX_T &&
+                sizeof(typename CarryTraits<S, Op>::C) <= 16) {
     if (const uint32_t lag = scan_lag(); lag && src_stride == 1 && dst_stride == 1) {
       constexpr uint64_t kTile = uint64_t(kScanThreads) * smem_scan_items<T>();
       using LW = LagWs<T, S, Op>;
