@@ -751,6 +751,8 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   unsigned char* buf =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
   const unsigned lane = lane_id(), warp = threadIdx.x / kWarp;
+  uint64_t* const tr = a.trace;  // FORGE_DEV builds: per-ticket phase stamps (tools/trace_lag.py)
+  const uint64_t t_start = tr ? global_ns() : 0;
 
   // ---- claim; the A load is issued speculatively for blockIdx.x first
   if (threadIdx.x == 0) {
@@ -785,6 +787,10 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   __syncthreads();
   const uint32_t k = s_k, epoch = s_epoch;
   uint32_t phase = s_phase;
+  if (tr && threadIdx.x == 0) {
+    tr[uint64_t(k) * 8 + 0] = t_start;
+    tr[uint64_t(k) * 8 + 1] = global_ns();
+  }
   const bool hasA = k < a.ntiles;
   const bool hasB = k >= L.lag && k - L.lag < a.ntiles;
   const uint64_t j = uint64_t(k) - L.lag;  // B's tile
@@ -862,12 +868,14 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     carry = opt_combine(cop, carry, grp_carry);
     carry = opt_combine(cop, carry, ing);
     if (lane == 0) s_carry = carry;
+    if (tr && lane == 0) tr[uint64_t(k) * 8 + 4] = global_ns();
   }
 
   // ---- A: fold tile k, publish its aggregate
   if (hasA) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
+    if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 2] = global_ns();
     Opt<A> tot;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -898,6 +906,7 @@ __global__ void __launch_bounds__(kScanThreads, 6)
           while (global_ns() - t0 < a.perturb_ns) __nanosleep(200);
         }
         IO::write(L.tagg, k, IO::GW, epoch, kPartial, M::to_c(w.v));  // compact: tile k at k * ST words
+        if (tr) tr[uint64_t(k) * 8 + 3] = global_ns();
       }
     }
     __syncthreads();
@@ -940,6 +949,7 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     tma_load_2d_hint(buf, &tmap, 0, int(j) * kScanThreads, &bar, l2_policy_evict_first());
   }
   mbar_wait(&bar, phase);
+  if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 5] = global_ns();
   Opt<A> tot;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
@@ -1038,9 +1048,11 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   fence_proxy_async_smem();
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (tr) tr[uint64_t(k) * 8 + 6] = global_ns();
     tma_store_2d_hint(&tmap_out, 0, int(j) * kScanThreads, buf, l2_policy_evict_first());
     tma_store_commit();
     tma_store_wait_read();
+    if (tr) tr[uint64_t(k) * 8 + 7] = global_ns();
   }
 }
 
@@ -1216,6 +1228,9 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                                reinterpret_cast<uint64_t*>(w + LW::gstate_off(nfull)), lag,
                                uint32_t(nfull + lag)};
         L.s.ntiles = uint32_t(nfull);
+#ifdef FORGE_DEV
+        L.s.trace = scan_trace_for(nfull + lag);
+#endif
         S* full_total = reinterpret_cast<S*>(w + LW::total_off(nfull));
         L.s.total_out = tail ? full_total : total_out;
         if (const cudaError_t e = ws_claim(ws, kWsTagScanLag, LW::tail_off(nfull), stream); e != cudaSuccess) return e;
