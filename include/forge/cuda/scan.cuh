@@ -1220,7 +1220,11 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
       const uint64_t nfull = n / kTile;
       const uint64_t tail = n - nfull * kTile;
       CUtensorMap tin, tout;
-      if (nfull >= 4 * kLagGroup && nfull + lag < (1ull << 31) && ws_bytes >= LW::bytes(nfull, kTile) &&
+      // below ~3 lags of full tiles the single-pass kernel is faster (the lag's
+      // A-only / B-only tickets dominate; CUDA-graph f32: 2^20 6.4 vs 11.3 us,
+      // 2^23 18.3 vs 19.6, 2^24 39.3 vs 37.1, 2^26 120 vs 113)
+      if (nfull >= 3ull * lag && nfull >= 4 * kLagGroup && nfull + lag < (1ull << 31) &&
+          ws_bytes >= LW::bytes(nfull, kTile) &&
           make_rows128_map(&tin, src, nfull * kTile * sizeof(T) / kRowBytes, uint32_t(kScanThreads)) &&
           make_rows128_map(&tout, dst, nfull * kTile * sizeof(S) / kRowBytes, uint32_t(kScanThreads))) {
         char* w = static_cast<char*>(ws);

@@ -1,9 +1,10 @@
 """The lagged scan (include/forge/cuda/scan.cuh scan_lag_kernel, the default
-for contiguous scans of >= 128 full tiles with sizeof(T) = sizeof(S) <= 16 and
-carries <= 16 bytes) at its boundaries, against the CPU oracle:
+for contiguous scans of >= 3 lags of full tiles (3 x 3.5 tiles per SM) with
+sizeof(T) = sizeof(S) <= 16 and carries <= 16 bytes) at its boundaries,
+against the CPU oracle:
 
-* the full-tile threshold (127 / 128 / 129 tiles) and full-tile counts below,
-  at and above the lag D (every ticket A-only then B-only; mixed);
+* the full-tile threshold (one below / at / above) and larger counts, plus
+  sizes below it (the single-pass kernel);
 * a partial last tile (the tail launch seeded with the full tiles' total);
 * carry_in and total_out through the device-pointer layer (the sharded
   scan's carry), inclusive and exclusive;
@@ -25,6 +26,15 @@ torch = pytest.importorskip("torch")
 capi = pytest.importorskip("paper_2603_18695_b200.capi")
 dev = pytest.importorskip("paper_2603_18695_b200.dev")
 F = pytest.importorskip("paper_2603_18695_b200.forge")
+
+
+def lag_tiles():
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    return sms * 7 // 2
+
+
+def threshold():
+    return 3 * lag_tiles()
 
 
 def tile_elems(op):
@@ -50,9 +60,10 @@ def run(op, inclusive, x, ws, carry=None, want_total=False):
 
 
 @pytest.mark.parametrize("op", [capi.I32_SUM, capi.F32_SUM, capi.ARGMAX_F32I32, capi.MAT2_U32])
-@pytest.mark.parametrize("tiles,extra", [(127, 0), (128, 0), (129, 5), (300, 0), (518, 1), (700, 4097), (1500, 3)])
+@pytest.mark.parametrize("dt,extra", [(-1, 0), (0, 0), (1, 5), (500, 4097), (2000, 3), (-1000, 7)])
 @pytest.mark.parametrize("inclusive", [True, False])
-def test_lag_thresholds_and_tails(op, tiles, extra, inclusive):
+def test_lag_thresholds_and_tails(op, dt, extra, inclusive):
+    tiles = threshold() + dt
     n = tiles * tile_elems(op) + extra
     x = orc.fill(op, n, 0x7A0 + tiles + extra)
     got, _ = run(op, inclusive, x, dev.Workspace())
@@ -64,7 +75,7 @@ def test_lag_thresholds_and_tails(op, tiles, extra, inclusive):
 @pytest.mark.parametrize("inclusive", [True, False])
 @pytest.mark.parametrize("extra", [0, 777])
 def test_lag_carry_in_and_total_out(op, inclusive, extra):
-    n = 600 * tile_elems(op) + extra
+    n = (threshold() + 50) * tile_elems(op) + extra
     x = orc.fill(op, n, 0x7B0 + op)
     c = orc.fill(op, 1, 0x7B1)[0]
     got, tot = run(op, inclusive, x, dev.Workspace(), carry=c, want_total=True)
@@ -79,7 +90,9 @@ def test_lag_workspace_reuse_across_layouts():
     ws = dev.Workspace()
     op = capi.I32_SUM
     te = tile_elems(op)
-    for tiles, extra in [(900, 11), (200, 7), (900, 11), (129, 1), (2000, 3), (130, 0), (900, 11)]:
+    t0 = threshold()
+    for tiles, extra in [(t0 + 300, 11), (200, 7), (t0 + 300, 11), (t0, 1), (t0 + 900, 3), (t0 + 1, 0),
+                         (t0 + 300, 11)]:
         n = tiles * te + extra
         x = orc.fill(op, n, 0x7C0 + tiles)
         for inclusive in (True, False):
@@ -91,7 +104,7 @@ def test_lag_workspace_reuse_across_layouts():
 def test_quaternion_single_pass_beside_lagged():
     # 32-byte f64 carry: the single-pass kernel (the lagged one spills)
     op = capi.QUAT_F32
-    n = 300 * tile_elems(op) + 9
+    n = (threshold() + 10) * tile_elems(op) + 9
     x = orc.fill(op, n, 0x7D0)
     got, _ = run(op, True, x, dev.Workspace())
     want, ex, sc = orc.scan(op, True, x)

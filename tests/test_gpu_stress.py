@@ -66,8 +66,9 @@ def test_mapreduce_relaunch_stress():
     assert np.all(got == want)
 
 
+@pytest.mark.parametrize("path", ["single_pass", "lagged"])
 @pytest.mark.parametrize("op", [capi.I32_SUM, capi.MAT2_U32, capi.F32_SUM])
-def test_relaxed_protocol_mutant_is_caught(op):
+def test_relaxed_protocol_mutant_is_caught(op, path):
     # The ordering ablation (MutationFlags::relax_scan_flag,
     # reference primitives.hpp:64-67): with the epoch tag of the tile states
     # ignored, a tile may accept a predecessor's state left by the PREVIOUS
@@ -79,8 +80,15 @@ def test_relaxed_protocol_mutant_is_caught(op):
     # seeded schedules.  Two inputs alternate on one workspace; every output is
     # checked bit for bit.  The product protocol must pass under the same
     # schedule, the mutant must be caught.
+    # path "lagged": above the lagged scan's threshold (3 lags of 3.5 tiles per
+    # SM, include/forge/cuda/scan.cuh), whose A phases publish the aggregates
+    # the mutant may confuse with the previous launch's
     lib = capi.load()
-    n = (1 << 22) + 17
+    if path == "single_pass":
+        n = (1 << 22) + 17
+    else:
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        n = (3 * (sms * 7 // 2) + 100) * (32768 // F.op_info(op)["t_size"]) + 17
     xs, want = [], []
     ws = dev.Workspace()
     # the two seeds differ above bit 40: element i of the generator depends on
