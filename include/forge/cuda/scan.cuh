@@ -104,6 +104,14 @@ struct TileStateIO {
 #pragma unroll
     for (int i = 0; i < GW; i += 4) ld_relaxed_gpu_v4(p + i, raw[i], raw[i + 1], raw[i + 2], raw[i + 3]);
   }
+  // The state's kind from its tags alone (value not decoded); 0 = INVALID.
+  static __device__ __forceinline__ uint32_t kind_of(const uint64_t* raw, uint32_t epoch) {
+    const uint32_t hi = uint32_t(raw[0] >> 32);
+    bool same = true;
+#pragma unroll
+    for (int i = 1; i < SW; ++i) same &= uint32_t(raw[i] >> 32) == hi;
+    return same && (hi >> 2) == (epoch & 0x3fffffffu) ? hi & 3u : 0u;
+  }
   // Decodes the state at word offset `off` of a group; 0 = INVALID.
   static __device__ __forceinline__ uint32_t decode(const uint64_t* raw, uint32_t epoch, C& v,
                                                    uint32_t epoch_mask = 0x3fffffffu) {
@@ -161,6 +169,7 @@ struct ScanTestHooks {
   bool relax_epoch = false;
   uint64_t perturb_seed = 0;
   uint32_t perturb_ns = 0;
+  bool ring_bypass = false;  // lagged scan: B ignores the row-prefix ring and folds every tile itself
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -699,10 +708,21 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
 //             folds the group's 32 aggregates and publishes the group
 //             aggregate (group state kind PARTIAL).
 //   B(k - D)  the scan of tile j = k - D, D tiles behind: re-load it (an L2 hit:
-//             D tiles of reads + writes stay well inside the 126 MB L2), fold
-//             its rows, compose with the tile's exclusive prefix, emit, TMA
+//             D tiles of reads + writes stay well inside the 126 MB L2),
+//             compose each row's exclusive prefix with the tile's, emit, TMA
 //             store; the last tile of a group publishes the group's inclusive
 //             prefix (group state kind PREFIX).
+// Row prefixes: A(k) has every row's exclusive prefix inside the tile (its
+// block scan) and leaves them in a RING slot (slot k mod R, R = 2048 >> D plus
+// the spread of resident tickets); B(k - D) reads its row's prefix there
+// instead of folding the tile a second time (one pass over the tile in B, not
+// two).  No flags, no fences, no waits: every 32-bit chunk of an entry travels
+// in a 64-bit word {tag, chunk} (single-copy atomic, relaxed .gpu accesses),
+// tag = f(epoch, lap of the slot), so each thread validates its own entry; if
+// any entry of the tile is not A(j)'s (A(j) not yet visible, or already
+// overwritten by A(j + R)), the CTA folds the tile itself with A's exact code
+// (same tree, same bits).  B then drops the slot's dead lines from L2
+// (discard: no write-back of scratch that is never read again).
 // j's exclusive prefix needs only states published by LOWER tickets' A phases
 // (tile aggregates of j's group, group aggregates) plus, as a shortcut, group
 // PREFIXes of finished B phases: warp 0 reads them — one 32-lane round of
@@ -721,8 +741,70 @@ struct LagArgs {
   ScanArgs<T, S, F, Op> s;  // src, dst, f, op, identity, carry_in, total_out, ctrl, ntiles (full tiles)
   uint64_t* tagg;           // tile aggregates: STRIDE words per tile, compact
   uint64_t* gstate;         // group states: STRIDE words per group, compact
+  uint64_t* ring;           // ring slots: kScanThreads tagged row prefixes each
+  uint32_t ring_slots;      // R = min(ntiles, kLagRing)
+  uint32_t ring_flags;      // kRingDiscard | kRingBypass (test hook: B always folds)
   uint32_t lag;             // D
   uint32_t nclaims;         // ntiles + D
+};
+
+constexpr uint32_t kLagRing = 2048;  // row-prefix ring slots (> D + resident tickets)
+constexpr uint32_t kRingDiscard = 1, kRingBypass = 2;
+// Ring entry tag: the epoch and the lap of the slot (tile / R mod 4: a slot
+// holds lap L - 1, L or L + 1 of this launch, or older launches' entries),
+// complemented so a zeroed workspace never matches.
+__device__ __forceinline__ uint32_t ring_tag(uint32_t epoch, uint32_t tile, uint32_t slots) {
+  return ~(((epoch & 0x3fffffffu) << 2) | ((tile / slots) & 3u));
+}
+// Whether the lagged scan keeps the row-prefix ring (Op::kLagRowPrefixRing
+// overrides).  Measured on B200 at 2^28 (GB/s, ring vs B folding its tile):
+// argmax (8-byte A) 4,950 vs 4,500; f32 / i32 sums (4-byte A) 5,330 vs 5,320 /
+// 5,220 vs 5,240 (the fold is cheap); affine (16-byte f64 A: 8 KB of tagged
+// entries per tile) 4,490 vs 4,990 and Mat2 4,780 vs 4,960 (the ring's L2
+// footprint costs more re-read hits than the fold it saves).
+template <class Op, class = void>
+struct LagRingOverride {
+  static constexpr int value = -1;
+};
+template <class Op>
+struct LagRingOverride<Op, std::void_t<decltype(Op::kLagRowPrefixRing)>> {
+  static constexpr int value = Op::kLagRowPrefixRing ? 1 : 0;
+};
+template <class S, class Op>
+constexpr bool lag_ring() {
+  constexpr int o = LagRingOverride<Op>::value;
+  return o >= 0 ? o == 1 : sizeof(typename ScanMath<S, Op>::A) == 8;
+}
+
+template <class A>
+struct RingIO {
+  static constexpr int W = Words<A>::N;  // 64-bit words per entry
+  static_assert(W == 1 || W == 2 || W == 4, "ring entries of 4, 8 or 16 bytes");
+  static __device__ __forceinline__ void write(uint64_t* e, uint32_t tag, const A& v) {
+    const Words<A> w = to_words(v);
+    const uint64_t hi = uint64_t(tag) << 32;
+    if constexpr (W == 1) {
+      st_relaxed_gpu(e, hi | w.w[0]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < W; i += 2) st_relaxed_gpu_v2(e + i, hi | w.w[i], hi | w.w[i + 1]);
+    }
+  }
+  static __device__ __forceinline__ bool read(const uint64_t* e, uint32_t tag, A& v) {
+    uint64_t raw[W];
+    if constexpr (W == 1) raw[0] = ld_relaxed_gpu(e);
+    else if constexpr (W == 2) ld_relaxed_gpu_v2(e, raw[0], raw[1]);
+    else ld_relaxed_gpu_v4(e, raw[0], raw[1], raw[2], raw[3]);
+    bool ok = true;
+    Words<A> w;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      ok &= uint32_t(raw[i] >> 32) == tag;
+      w.w[i] = uint32_t(raw[i]);
+    }
+    v = from_words<A>(w);
+    return ok;
+  }
 };
 
 template <class T, class S, class F, class Op, bool Inclusive>
@@ -738,7 +820,6 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   constexpr int EPC = 16 / int(sizeof(T));
   constexpr int NCH = kRowBytes / 16;
   constexpr int NW = kScanThreads / kWarp;
-  constexpr uint64_t kTile = uint64_t(kScanThreads) * IT;
   const auto& a = L.s;
   extern __shared__ unsigned char dyn_smem[];
   __shared__ __align__(8) uint64_t bar;
@@ -746,6 +827,7 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   __shared__ Opt<A> s_warp[NW];
   __shared__ Opt<C> s_carry;
   __shared__ C s_carry_agg;  // A's tile aggregate
+  __shared__ C s_self_agg;   // B's tile aggregate (published by A(j))
   auto aop = [&](const A& x, const A& y) { return M::comb(a.op, x, y); };
   auto cop = [&](const C& x, const C& y) { return M::CT::op(a.op, x, y); };
   unsigned char* buf =
@@ -799,12 +881,20 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   if (hasB && warp == 0) {
     const uint64_t grp = j / kLagGroup;
     const uint32_t r = uint32_t(j % kLagGroup);
+    // B publishes the group PREFIX (last tile of a group) / the total (last
+    // tile): it needs tile j's own aggregate too (lane r)
+    const bool want_self = r == kLagGroup - 1 || j == a.ntiles - 1;
     Opt<C> carry{C{}, false};
-    // in-group: aggregates of tiles grp*32 .. j-1 (lane l: tile grp*32 + l)
+    // in-group: aggregates of tiles grp*32 .. j-1 (lane l: tile grp*32 + l).
+    // The group's state has two writers — A(j) of its last tile (PARTIAL) and
+    // B of that tile (PREFIX, below) — so B waits until A's PARTIAL is in
+    // (lane 0): a state wider than one 128-bit store could otherwise end up
+    // torn between the two (a permanently invalid state: measured as a rare
+    // hang with 16-byte carries), and a late PARTIAL would hide the PREFIX.
     Opt<C> ing{C{}, false};
     {
       C v{};
-      bool ok = lane >= r;
+      bool ok = !(lane < r || (lane == r && want_self));
       while (true) {
         if (!ok) {
           uint64_t raw[ST];
@@ -818,6 +908,20 @@ __global__ void __launch_bounds__(kScanThreads, 6)
         }
         if (__all_sync(kFullMask, ok)) break;
       }
+      if (r == kLagGroup - 1 && lane == 0) {  // (usually in long before: A(j) ran D tickets ago)
+        while (true) {
+          uint64_t raw[ST];
+          const uint64_t* p = L.gstate + grp * ST;
+#pragma unroll
+          for (int i = 0; i < ST; i += 2) {
+            if constexpr (ST == 1) raw[0] = ld_relaxed_gpu(p);
+            else ld_relaxed_gpu_v2(p + i, raw[i], raw[i + 1]);
+          }
+          if (IO::kind_of(raw, epoch) == kPartial) break;  // this launch's (never the relaxed-epoch test mask)
+        }
+      }
+      __syncwarp();
+      if (want_self && lane == r) s_self_agg = v;
       Opt<C> x{v, lane < r};
       // ordered fold of lanes 0..r-1 (lane order = tile order)
 #pragma unroll
@@ -871,14 +975,13 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     if (tr && lane == 0) tr[uint64_t(k) * 8 + 4] = global_ns();
   }
 
-  // ---- A: fold tile k, publish its aggregate
-  if (hasA) {
-    mbar_wait(&bar, phase);
-    phase ^= 1u;
-    if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 2] = global_ns();
+  constexpr bool kRing = lag_ring<S, Op>();
+  // The tile in `buf` folded: this row's exclusive prefix inside the tile,
+  // (warps before) o (lanes before); s_warp[NW - 1] = the tile aggregate.
+  // A(k) and B's fallback run exactly this code, so both give the same bits.
+  auto tile_row_prefix = [&](auto want_row, auto sync_first, auto&& on_aggregate) -> Opt<A> {
     Opt<A> tot;
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    auto fold_chunk = [&](int c) {
       const uint4 v = lds128(buf + swz128(threadIdx.x, c));
       T x[EPC];
       memcpy(x, &v, 16);
@@ -887,29 +990,59 @@ __global__ void __launch_bounds__(kScanThreads, 6)
         const A y = M::lift(a.f(x[e]));
         tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
       }
+    };
+    if constexpr (sizeof(A) >= 16) {  // wide accumulators: fewer row chunks in flight (no spill at 40 registers)
+#pragma unroll 2
+      for (int c = 0; c < NCH; ++c) fold_chunk(c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) fold_chunk(c);
     }
     tot.has = true;
-    tot = warp_scan_incl(aop, tot);
-    if (lane == kWarp - 1) s_warp[warp] = tot;
+    const Opt<A> incl = warp_scan_incl(aop, tot);
+    if constexpr (decltype(sync_first)::value) __syncthreads();  // s_warp: earlier readers are done
+    if (lane == kWarp - 1) s_warp[warp] = incl;
     __syncthreads();
-    // the tile aggregate by the SAME tree as B's block scan below (warp scan of
-    // the warp totals), so A's published aggregate and the aggregate B folds
-    // into its group PREFIX are the same bits: the carry a tile gets does not
-    // depend on which of the two the look-back found
     if (warp == 0) {
       Opt<A> w = lane < NW ? s_warp[lane] : Opt<A>{A{}, false};
       w = warp_scan_incl(aop, w);
-      if (lane == NW - 1) {
-        s_carry_agg = M::to_c(w.v);
-        if (a.perturb_ns && ((uint64_t(k) * 0x9E3779B97F4A7C15ull) ^ a.perturb_seed) % 8 == 0) {  // test hook
-          const uint64_t t0 = global_ns();
-          while (global_ns() - t0 < a.perturb_ns) __nanosleep(200);
-        }
-        IO::write(L.tagg, k, IO::GW, epoch, kPartial, M::to_c(w.v));  // compact: tile k at k * ST words
-        if (tr) tr[uint64_t(k) * 8 + 3] = global_ns();
+      if constexpr (decltype(want_row)::value) {
+        if (lane < NW) s_warp[lane] = w;
       }
+      if (lane == NW - 1) on_aggregate(w.v);  // the tile aggregate
     }
     __syncthreads();
+    if constexpr (decltype(want_row)::value) {
+      const Opt<A> warp_ex = warp > 0 ? s_warp[warp - 1] : Opt<A>{A{}, false};
+      Opt<A> lane_ex = shfl_up_opt(incl, 1);
+      if (lane == 0) lane_ex.has = false;
+      return opt_combine(aop, warp_ex, lane_ex);
+    } else {
+      return Opt<A>{A{}, false};
+    }
+  };
+  const uint32_t R = L.ring_slots;
+  constexpr int RW = RingIO<A>::W;
+
+  // ---- A: fold tile k, publish its aggregate, leave its row prefixes in the ring
+  if (hasA) {
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 2] = global_ns();
+    const Opt<A> row_ex =
+        tile_row_prefix(std::bool_constant<kRing>{}, std::false_type{}, [&](const A& total) {
+          const C agg = M::to_c(total);
+          s_carry_agg = agg;
+          if (a.perturb_ns && ((uint64_t(k) * 0x9E3779B97F4A7C15ull) ^ a.perturb_seed) % 8 == 0) {  // test hook
+            const uint64_t t0 = global_ns();
+            while (global_ns() - t0 < a.perturb_ns) __nanosleep(200);
+          }
+          IO::write(L.tagg, k, IO::GW, epoch, kPartial, agg);  // compact: tile k at k * ST words
+          if (tr) tr[uint64_t(k) * 8 + 3] = global_ns();
+        });
+    if (kRing && threadIdx.x > 0)
+      RingIO<A>::write(L.ring + (uint64_t(k % R) * kScanThreads + threadIdx.x) * RW, ring_tag(epoch, k, R),
+                       row_ex.v);
     // the last tile of a group publishes the group aggregate (warp 1: it polls
     // the group's other 31 aggregates, published by lower tickets)
     if (k % kLagGroup == kLagGroup - 1 && warp == 1) {
@@ -939,54 +1072,38 @@ __global__ void __launch_bounds__(kScanThreads, 6)
       if (lane == 0) IO::write(L.gstate, grp, IO::GW, epoch, kPartial, x.v);
     }
   }
+  __syncthreads();  // every read of A's tile is done (and s_carry / s_self_agg are visible)
   if (!hasB) return;
 
-  // ---- B: re-load tile j (L2), scan it with the carry, store
-  __syncthreads();  // every read of A's tile is done (and s_carry is visible)
+  // ---- B: re-load tile j (L2) and its row prefixes (ring), emit, store
   if (threadIdx.x == 0) {
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&bar, kSmemTileBytes);
     tma_load_2d_hint(buf, &tmap, 0, int(j) * kScanThreads, &bar, l2_policy_evict_first());
   }
+  const uint64_t* const slot = L.ring + uint64_t(uint32_t(j) % R) * kScanThreads * RW;
+  Opt<A> row_ex{A{}, threadIdx.x > 0};
+  bool ring_ok = kRing && !(L.ring_flags & kRingBypass);
+  if (ring_ok && threadIdx.x > 0)
+    ring_ok = RingIO<A>::read(slot + threadIdx.x * RW, ring_tag(epoch, uint32_t(j), R), row_ex.v);
   mbar_wait(&bar, phase);
   if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 5] = global_ns();
-  Opt<A> tot;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const uint4 v = lds128(buf + swz128(threadIdx.x, c));
-    T x[EPC];
-    memcpy(x, &v, 16);
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) {
-      const A y = M::lift(a.f(x[e]));
-      tot.v = (c == 0 && e == 0) ? y : aop(tot.v, y);
-    }
+  // an entry that is not A(j)'s (not yet visible, or already overwritten by
+  // A(j + R)), or no ring: the CTA folds the tile itself
+  if constexpr (kRing) {
+    if (!__syncthreads_and(ring_ok)) row_ex = tile_row_prefix(std::true_type{}, std::true_type{}, [](const A&) {});
+  } else {
+    row_ex = tile_row_prefix(std::true_type{}, std::true_type{}, [](const A&) {});
   }
-  tot.has = true;
-  Opt<A> incl = warp_scan_incl(aop, tot);
-  __syncthreads();  // s_warp reuse: A's readers are done
-  if (lane == kWarp - 1) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    Opt<A> w = lane < NW ? s_warp[lane] : Opt<A>{A{}, false};
-    w = warp_scan_incl(aop, w);
-    if (lane < NW) s_warp[lane] = w;
-  }
-  __syncthreads();
   const Opt<C> carry = s_carry;
   if (threadIdx.x == 0 && (j % kLagGroup == kLagGroup - 1 || j == a.ntiles - 1)) {
-    const C pre = carry.has ? cop(carry.v, M::to_c(s_warp[NW - 1].v)) : M::to_c(s_warp[NW - 1].v);
+    const C agg = s_self_agg;  // tile j's aggregate (A(j)'s, read by the look-back)
+    const C pre = carry.has ? cop(carry.v, agg) : agg;
     if (j % kLagGroup == kLagGroup - 1) IO::write(L.gstate, j / kLagGroup, IO::GW, epoch, kPrefix, pre);
     if (j == a.ntiles - 1 && a.total_out) *a.total_out = M::CT::to_s(pre);
   }
-  Opt<A> run;
-  {
-    const Opt<A> warp_ex = warp > 0 ? s_warp[warp - 1] : Opt<A>{A{}, false};
-    Opt<A> lane_ex = shfl_up_opt(incl, 1);
-    if (lane == 0) lane_ex.has = false;
-    const Opt<A> tile_ex = carry.has ? Opt<A>{M::from_c(carry.v), true} : Opt<A>{A{}, false};
-    run = opt_combine(aop, opt_combine(aop, tile_ex, warp_ex), lane_ex);
-  }
+  const Opt<A> tile_ex = carry.has ? Opt<A>{M::from_c(carry.v), true} : Opt<A>{A{}, false};
+  const Opt<A> run = opt_combine(aop, tile_ex, row_ex);
   using E = std::conditional_t<M::kNarrowEmit, S, A>;
   Opt<E> em;
   if constexpr (M::kNarrowEmit)
@@ -1046,13 +1163,20 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   else
     emit_rows(std::false_type{});
   fence_proxy_async_smem();
-  __syncthreads();
+  __syncthreads();  // every row prefix of the slot has been read and used
   if (threadIdx.x == 0) {
     if (tr) tr[uint64_t(k) * 8 + 6] = global_ns();
     tma_store_2d_hint(&tmap_out, 0, int(j) * kScanThreads, buf, l2_policy_evict_first());
     tma_store_commit();
     tma_store_wait_read();
     if (tr) tr[uint64_t(k) * 8 + 7] = global_ns();
+  } else if (kRing && warp == 1 && (L.ring_flags & kRingDiscard)) {
+    // the slot's lines are dead (read once): drop them from L2 without a
+    // write-back.  A hint only — an entry lost to a late discard reads as
+    // not-A(j)'s and its tile is folded by B.
+    constexpr uint32_t kSlotLines = uint32_t(kScanThreads * RW * 8) / 128u;
+#pragma unroll
+    for (uint32_t i = lane; i < kSlotLines; i += kWarp) discard_l2_line(reinterpret_cast<const char*>(slot) + i * 128u);
   }
 }
 
@@ -1079,7 +1203,10 @@ struct ScanWs {
       sizeof(S) >= 16 ? 2 * uint64_t(kScanThreads) * (kRowBytes / 16)
                       : uint64_t(kScanThreads) * (sizeof(S) <= uint64_t(kRowBytes) ? kRowBytes / sizeof(S) : 1);
   static uint64_t min_bytes_for(uint64_t tiles) { return 256 + IO::slots(tiles ? tiles : 1) * kMinSlotWords * 8; }
-  static uint64_t bytes(uint64_t n) {
+  // full-speed bytes for n items: the single-pass kernels' states, or the
+  // lagged kernel's layout (LagWs) when it takes the scan, whichever is larger
+  static uint64_t bytes(uint64_t n);
+  static uint64_t base_bytes(uint64_t n) {
     const uint64_t full = 256 + IO::slots(n ? ceil_div(n, kSizedTile) : 1) * kSlotWords * 8;
     const uint64_t packed = min_bytes_for(ceil_div(n, kTileGeneral));
     return full > packed ? full : packed;
@@ -1094,19 +1221,39 @@ struct ScanWs {
   static uint64_t claim_bytes(uint64_t tiles, uint32_t stride) { return 256 + IO::slots(tiles) * stride * 8; }
 };
 
+#ifndef FORGE_SCAN_LAG_MAX_T
+#define FORGE_SCAN_LAG_MAX_T 16  // largest element (bytes) taken by the lagged scan
+#endif
+
+// Lagged-scan workspace: [256-byte control block | ring slots (min(tiles,
+// kLagRing) x 256 tagged row prefixes) | tile
+// aggregates | group states | full-tile total | tail sub-workspace].
 template <class T, class S, class Op>
 struct LagWs {
   using C = typename CarryTraits<S, Op>::C;
+  using A = typename ScanMath<S, Op>::A;
   static constexpr uint64_t ST = uint64_t(TileStateIO<C>::STRIDE);
   static constexpr uint64_t align(uint64_t v) { return (v + 255) & ~uint64_t(255); }
-  static uint64_t tagg_off() { return 256; }
-  static uint64_t gstate_off(uint64_t tiles) { return tagg_off() + align(tiles * ST * 8); }
+  static uint64_t ring_slots(uint64_t tiles) { return tiles < kLagRing ? tiles : kLagRing; }
+  static constexpr uint64_t kSlotBytes =  // tagged entries
+      lag_ring<S, Op>() ? uint64_t(kScanThreads) * RingIO<A>::W * 8 : 0;
+  static uint64_t ring_off() { return 256; }
+  static uint64_t tagg_off(uint64_t tiles) { return ring_off() + align(ring_slots(tiles) * kSlotBytes); }
+  static uint64_t gstate_off(uint64_t tiles) { return tagg_off(tiles) + align(tiles * ST * 8); }
   static uint64_t total_off(uint64_t tiles) { return gstate_off(tiles) + align(ceil_div(tiles, kLagGroup) * ST * 8); }
   static uint64_t tail_off(uint64_t tiles) { return total_off(tiles) + 256; }
+  // the tail launch (< one tile) never takes the lagged kernel
   static uint64_t bytes(uint64_t tiles, uint64_t tile_items) {
-    return tail_off(tiles) + ScanWs<T, S, Op>::bytes(tile_items);
+    return tail_off(tiles) + ScanWs<T, S, Op>::base_bytes(tile_items);
   }
 };
+
+template <class T, class S, class Op>
+constexpr bool lag_scan_type_ok() {
+  return smem_scan_type_ok<T>() && sizeof(S) == sizeof(T) && sizeof(T) <= FORGE_SCAN_LAG_MAX_T &&
+         sizeof(typename CarryTraits<S, Op>::C) <= 16;
+}
+
 
 // Development knobs (FORGE_DEV builds only; constants otherwise).
 inline uint32_t scan_lookback_mode() {
@@ -1121,9 +1268,6 @@ inline bool scan_force_regs() {
   static const bool v = dev_knob("FORGE_SCAN_REGS", 0) != 0;
   return v;
 }
-#ifndef FORGE_SCAN_LAG_MAX_T
-#define FORGE_SCAN_LAG_MAX_T 16  // largest element (bytes) taken by the lagged scan
-#endif
 // Lag D of the lagged scan (scan_lag_kernel), in tiles; 0 = the single-pass
 // kernel.  Measured on B200 (148 SMs, f32 / i32 / affine / argmax at 2^28,
 // GB/s): D = 256: 4133 / 3744 / 3757 / 3401 (B waits for A's aggregates);
@@ -1132,6 +1276,12 @@ inline bool scan_force_regs() {
 // 4828 / 4849 / 4479 / 4517.  D scales with the resident tiles: 3.5 per SM.
 inline uint32_t scan_lag() {
   static const uint32_t v = dev_knob("FORGE_SCAN_LAG", device_props().sm_count * 7 / 2);
+  return v;
+}
+// kRingDiscard | kRingBypass (FORGE_DEV knob FORGE_SCAN_RING; kRingBypass is
+// also the test hook ScanTestHooks::ring_bypass)
+inline uint32_t scan_ring_flags() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_RING", kRingDiscard);
   return v;
 }
 inline bool scan_no_tma_store() {
@@ -1188,6 +1338,28 @@ inline uint64_t* scan_trace_for(uint64_t tiles) {
 }
 #endif
 
+// The lagged kernel takes contiguous scans of >= lag_min_tiles() full tiles
+// (below ~3 lags the single-pass kernel is faster: CUDA-graph f32 2^20 6.4 vs
+// 11.3 us, 2^23 18.3 vs 19.6, 2^24 39.3 vs 37.1, 2^26 120 vs 113).
+inline uint64_t lag_min_tiles() {
+  const uint64_t d = scan_lag();
+  return d ? (3 * d > 4 * kLagGroup ? 3 * d : 4 * kLagGroup) : ~uint64_t(0);
+}
+
+template <class T, class S, class Op>
+uint64_t ScanWs<T, S, Op>::bytes(uint64_t n) {
+  uint64_t b = base_bytes(n);
+  if constexpr (lag_scan_type_ok<T, S, Op>()) {
+    constexpr uint64_t kTile = uint64_t(kScanThreads) * smem_scan_items<T>();
+    const uint64_t tiles = n / kTile;
+    if (tiles >= lag_min_tiles()) {
+      const uint64_t lag = LagWs<T, S, Op>::bytes(tiles, kTile);
+      b = lag > b ? lag : b;
+    }
+  }
+  return b;
+}
+
 // Launch.  `ws` holds `ws_bytes` bytes (>= ScanWs::min_bytes_for(tiles) of the
 // kernel that runs; ScanWs::bytes(n) gives full-speed slots), zeroed once at
 // creation.  Returns cudaErrorInvalidValue when the workspace is too small
@@ -1212,24 +1384,25 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   // register kernel.
   // lagged scan: elements and carries of at most 16 bytes (a 32-byte f64
   // quaternion carry spills at 6 CTAs/SM: 3.20 TB/s lagged vs 3.57 single-pass)
-  if constexpr (smem_scan_type_ok<T>() && sizeof(S) == sizeof(T) && sizeof(T) <= FORGE_SCAN_LAG_MAX_T &&
-                sizeof(typename CarryTraits<S, Op>::C) <= 16) {
+  if constexpr (lag_scan_type_ok<T, S, Op>()) {
     if (const uint32_t lag = scan_lag(); lag && src_stride == 1 && dst_stride == 1) {
       constexpr uint64_t kTile = uint64_t(kScanThreads) * smem_scan_items<T>();
       using LW = LagWs<T, S, Op>;
       const uint64_t nfull = n / kTile;
       const uint64_t tail = n - nfull * kTile;
       CUtensorMap tin, tout;
-      // below ~3 lags of full tiles the single-pass kernel is faster (the lag's
-      // A-only / B-only tickets dominate; CUDA-graph f32: 2^20 6.4 vs 11.3 us,
-      // 2^23 18.3 vs 19.6, 2^24 39.3 vs 37.1, 2^26 120 vs 113)
-      if (nfull >= 3ull * lag && nfull >= 4 * kLagGroup && nfull + lag < (1ull << 31) &&
+      if (nfull >= lag_min_tiles() && nfull + lag < (1ull << 30) &&
           ws_bytes >= LW::bytes(nfull, kTile) &&
           make_rows128_map(&tin, src, nfull * kTile * sizeof(T) / kRowBytes, uint32_t(kScanThreads)) &&
           make_rows128_map(&tout, dst, nfull * kTile * sizeof(S) / kRowBytes, uint32_t(kScanThreads))) {
         char* w = static_cast<char*>(ws);
-        LagArgs<T, S, F, Op> L{a, reinterpret_cast<uint64_t*>(w + LW::tagg_off()),
-                               reinterpret_cast<uint64_t*>(w + LW::gstate_off(nfull)), lag,
+        LagArgs<T, S, F, Op> L{a,
+                               reinterpret_cast<uint64_t*>(w + LW::tagg_off(nfull)),
+                               reinterpret_cast<uint64_t*>(w + LW::gstate_off(nfull)),
+                               reinterpret_cast<uint64_t*>(w + LW::ring_off()),
+                               uint32_t(LW::ring_slots(nfull)),
+                               scan_ring_flags() | (hooks.ring_bypass ? kRingBypass : 0u),
+                               lag,
                                uint32_t(nfull + lag)};
         L.s.ntiles = uint32_t(nfull);
 #ifdef FORGE_DEV

@@ -271,7 +271,14 @@ inline uint64_t b200_state_group_tiles(uint32_t accum_size) {  // tile states pe
   const uint64_t words = b200_state_min_bytes(accum_size) / 8;
   return words <= 4 ? 4 / words : 1;
 }
-inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
+inline uint64_t b200_sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    sms = 148;
+  return uint64_t(sms);
+}
+inline uint64_t b200_scan_ws_base(uint64_t n, uint32_t accum_size) {  // single-pass kernels
   const uint64_t P = b200_state_group_tiles(accum_size);
   const uint64_t sized_tiles = std::max<uint64_t>((n + b200_scan_sized_tile(accum_size) - 1) /
                                                       b200_scan_sized_tile(accum_size), 1);
@@ -283,12 +290,19 @@ inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
                               b200_state_min_bytes(accum_size);
   return std::max(full, packed);
 }
-inline uint64_t b200_sm_count() {
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-    sms = 148;
-  return uint64_t(sms);
+inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
+  uint64_t lag = 0;  // the lagged kernel's layout (cuda::LagWs) for a sizeof(S)-byte T
+  if (accum_size <= 16 && (accum_size & (accum_size - 1)) == 0) {
+    const uint64_t tile = 256 * (128 / accum_size);
+    const uint64_t tiles = n / tile;
+    if (tiles >= std::max<uint64_t>(3 * (b200_sm_count() * 7 / 2), 128)) {  // cuda::lag_min_tiles()
+      const uint64_t smb = b200_state_min_bytes(accum_size);
+      lag = 256 + rup(std::min<uint64_t>(tiles, 2048) * 256 * 4 * accum_size, 256) +  // tagged entries
+            rup(tiles * smb, 256) + rup((tiles + 31) / 32 * smb, 256) + 256 +
+            b200_scan_ws_base(tile, accum_size);
+    }
+  }
+  return std::max(b200_scan_ws_base(n, accum_size), lag);
 }
 inline uint64_t b200_mapreduce_ws_bytes(uint32_t accum_size) {
   const uint64_t grid = b200_sm_count() * 4;

@@ -14,8 +14,9 @@ from pathlib import Path
 
 # FORGE_LIB=dev selects libforge_dev.so (`make DEV=1`: the same kernels plus the
 # environment-read development knobs); the product is libforge.so.
-LIB_PATH = Path(__file__).resolve().parent / ("libforge_dev.so" if os.environ.get("FORGE_LIB") == "dev"
-                                              else "libforge.so")
+_lib_env = os.environ.get("FORGE_LIB", "")
+LIB_PATH = Path(__file__).resolve().parent / ("libforge_dev.so" if _lib_env == "dev"
+                                              else _lib_env if _lib_env.endswith(".so") else "libforge.so")
 
 # ---- status codes (forge_status) ------------------------------------------
 OK = 0
@@ -133,6 +134,7 @@ _SIGNATURES = {
     "forge_vcopy": (C.c_int, [_P, View, View, _u32, C.POINTER(ArchParams), C.POINTER(LaunchReport)]),
     "forge_set_mutation_flags": (C.c_int, [_i32, _i32]),
     "forge_set_schedule_perturbation": (C.c_int, [_u64, _u32]),
+    "forge_set_scan_ring_bypass": (C.c_int, [C.c_int32]),
     "forge_vload_pattern": (C.c_int, [_u64, _u32, C.POINTER(_u32), C.POINTER(_u32)]),
     "forge_dev_workspace_bytes": (C.c_int, [C.c_int, C.c_int, _u64, _u64, C.POINTER(_u64)]),
     "forge_dev_mapreduce": (C.c_int, [C.c_int, _P, _u64, _P, _P, _u64, _P]),
@@ -183,6 +185,8 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
                           f"`make -C paper_2603_18695_b200/csrc` (no CPU fallback exists)")
     lib = C.CDLL(str(p))
     for name, (res, args) in _SIGNATURES.items():
+        if _lib_env.endswith(".so") and not hasattr(lib, name):
+            continue  # FORGE_LIB=<other build>.so: development comparisons against older builds
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -110,3 +110,49 @@ def test_quaternion_single_pass_beside_lagged():
     want, ex, sc = orc.scan(op, True, x)
     assert_match(op, got, want, ex, sc, "quaternion scan")
     assert TOL[op] == 1e-5
+
+
+@pytest.mark.parametrize("op", [capi.F32_SUM, capi.I32_SUM, capi.AFFINE_F32, capi.ARGMAX_F32I32, capi.MAT2_U32])
+@pytest.mark.parametrize("inclusive", [True, False])
+def test_lag_ring_fallback_bit_identical(op, inclusive):
+    # B reads each row's exclusive prefix from the ring A left; a stale entry
+    # makes the CTA fold the tile itself with A's exact code.  With the ring
+    # bypassed (forge_set_scan_ring_bypass) every tile takes that fallback:
+    # the outputs must be the same BITS (floats included), and both equal the
+    # oracle.  Sizes above kLagRing = 2048 tiles wrap the ring (slot reuse).
+    lib = capi.load()
+    n = max(threshold() + 700, 2048 + 900) * tile_elems(op) + 13
+    x = orc.fill(op, n, 0x7E0 + op)
+    ws = dev.Workspace()
+    got, _ = run(op, inclusive, x, ws)
+    assert lib.forge_set_scan_ring_bypass(1) == 0
+    try:
+        byp, _ = run(op, inclusive, x, ws)
+        byp2, _ = run(op, inclusive, x, dev.Workspace())
+    finally:
+        lib.forge_set_scan_ring_bypass(0)
+    again, _ = run(op, inclusive, x, ws)
+    assert got.tobytes() == byp.tobytes() == byp2.tobytes() == again.tobytes()
+    want, ex, sc = orc.scan(op, inclusive, x)
+    assert_match(op, got, want, ex, sc, "lagged scan, ring")
+
+
+def test_lag_ops_alternating_on_one_workspace():
+    # lagged scans of different element / carry / ring-entry sizes alternate on
+    # one workspace (the ring and the tile states move with the layout); each
+    # output must equal its first (oracle-checked) launch bit for bit
+    ws = dev.Workspace()
+    ops = [capi.F32_SUM, capi.AFFINE_F32, capi.ARGMAX_F32I32, capi.MAT2_U32, capi.I32_SUM]
+    cases = {}
+    for op in ops:
+        n = (threshold() + 300) * tile_elems(op) + 5
+        x = orc.fill(op, n, 0x7F0 + op)
+        got, _ = run(op, True, x, ws)
+        want, ex, sc = orc.scan(op, True, x)
+        assert_match(op, got, want, ex, sc, "alternating")
+        cases[op] = (x, got)
+    for _ in range(3):
+        for op in ops:
+            x, first = cases[op]
+            got, _ = run(op, True, x, ws)
+            assert got.tobytes() == first.tobytes(), op

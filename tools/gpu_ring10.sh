@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 300 python tools/probe.py scan --check > gpurun_out/ring10.log 2>&1
+for op in 12 10 11; do timeout 60 python tools/hang_probe.py $op 400 27 >> gpurun_out/ring10.log 2>&1; done
+timeout 120 python tools/hang_probe2.py 40 28 >> gpurun_out/ring10.log 2>&1
+timeout 3000 python -m pytest tests -m gpu -q -x -p no:randomly > gpurun_out/pytest_ring10.log 2>&1; echo rc=$? >> gpurun_out/pytest_ring10.log
+exit 0
