@@ -132,3 +132,37 @@ def test_compute_sanitizer_clean(tool):
                         str(ROOT / "tools" / "sanitize_run.py")], cwd=ROOT, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "sanitize_run ok" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
+
+
+@pytest.mark.parametrize("op", [capi.MAT2_U32, capi.AFFINE_F32, capi.ARGMAX_F32I32])
+def test_lagged_scan_relaunch_watchdog(op):
+    # The lagged scan's group states have two writers (A's PARTIAL, B's
+    # PREFIX); with 16-byte carries their two 128-bit stores could once tear
+    # into a permanently invalid state — a hang every few hundred launches
+    # (Mat2 / affine at 2^27).  300 launches at that size under a host
+    # watchdog; every output equal to the first.  A hung kernel cannot be
+    # recovered from inside the process, so the watchdog ends it loudly.
+    import os
+    import time
+    n = (1 << 27) if F.op_info(op)["t_size"] <= 8 else (1 << 26)
+    ws = dev.Workspace()
+    x = dev.empty(op, n)
+    dev.fill_synthetic(op, x, n, 0x3A7C)
+    y = dev.empty(op, n, "S")
+    dev.scan(op, True, x, y, n, ws)
+    torch.cuda.synchronize()
+    first = y.clone()
+    ev = torch.cuda.Event()
+    for i in range(300):
+        dev.scan(op, True, x, y, n, ws)
+        ev.record()
+        t0 = time.time()
+        while not ev.query():
+            if time.time() - t0 > 10:
+                sys.stderr.write(f"lagged scan hung: op {op} launch {i}\n")
+                sys.stderr.flush()
+                os._exit(3)
+            time.sleep(0.0002)
+        if i % 50 == 49:
+            assert torch.equal(y, first), (op, i)
+    assert torch.equal(y, first)
