@@ -278,6 +278,11 @@ __device__ __forceinline__ uint64_t atom_add_acq_rel_gpu(uint64_t* p, uint64_t v
   asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(v) : "memory");
   return r;
 }
+__device__ __forceinline__ uint64_t atom_add_relaxed_gpu(uint64_t* p, uint64_t v) {
+  uint64_t r;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(v) : "memory");
+  return r;
+}
 __device__ __forceinline__ uint32_t atom_add_relaxed_gpu(uint32_t* p, uint32_t v) {
   uint32_t r;
   asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 300 python tools/probe.py scan --check > gpurun_out/persist.log 2>&1
+for L in libforge_old.so libforge.so; do FORGE_LIB=$L timeout 300 python tools/probe.py scan >> gpurun_out/persist.log 2>&1; done
+for op in 12 10 11 0; do timeout 60 python tools/hang_probe.py $op 400 27 >> gpurun_out/persist.log 2>&1; done
+timeout 120 python tools/hang_probe2.py 40 28 >> gpurun_out/persist.log 2>&1
+for op in 0 11; do timeout 120 python tools/trace_lag.py $op 28 >> gpurun_out/persist.log 2>&1; done
+timeout 1500 python -m pytest tests -m gpu -q -x -k "lag or stress or scan" -p no:randomly > gpurun_out/pytest_persist.log 2>&1; echo rc=$? >> gpurun_out/pytest_persist.log
+exit 0
