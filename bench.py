@@ -172,7 +172,7 @@ def kernel_of(kind, op):
     if kind == "mapreduce":
         return "mapreduce_kernel"
     if kind == "scan":
-        return "scan_smem_kernel"
+        return "scan_lag_kernel"  # 2^28-element scans: the lagged kernel (scan.cuh)
     if kind == "matvec":
         return "gevm_cols_kernel"
     return "gemv_kernel"
@@ -794,6 +794,13 @@ def context_breakdown(peaks) -> dict:
     dst = dev.empty(capi.F32_SUM, n1, "S")
     rec("scan_f32_sum_2^20_C1", n1 * 8, _time_dev(lambda: dev.scan(capi.F32_SUM, True, src, dst, n1, ws), 20),
         elems=n1, note="8 MiB, L2-resident: one call per event pair, host launch latency included")
+
+    def c1_calls():
+        for _ in range(100):
+            dev.scan(capi.F32_SUM, True, src, dst, n1, ws)
+    rec("scan_f32_sum_2^20_C1_back_to_back", n1 * 8, _time_dev(c1_calls, 5) / 100, elems=n1,
+        note="100 calls through the Python device-pointer layer between one event pair; per-call time "
+             "(max of the host call cost and the kernel)")
     try:
         gstream = torch.cuda.Stream()
         gstream.wait_stream(torch.cuda.current_stream())

@@ -10,7 +10,7 @@ fi
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench_rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "ref_rc=$?" >> gpurun_out/bench_ref.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-breakdown --no-c5 > gpurun_out/bench_ncu.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"scan_smem|mapreduce_kernel|gevm_cols|gemv_kernel|code_sum" -o /tmp/comp python tools/ncu_components.py run > gpurun_out/ncu_comp.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"scan_lag|scan_smem|mapreduce_kernel|gevm_cols|gemv_kernel|code_sum" -o /tmp/comp python tools/ncu_components.py run > gpurun_out/ncu_comp.log 2>&1
 ncu -i /tmp/comp.ncu-rep --page raw --csv > gpurun_out/comp_raw.csv 2>/dev/null
 ncu -i /tmp/comp.ncu-rep --page details --csv > gpurun_out/comp_details.csv 2>/dev/null
 python tools/ncu_components.py summarize gpurun_out/comp_raw.csv gpurun_out/r02_summary > gpurun_out/ncu_summary.log 2>&1

@@ -2,7 +2,7 @@
 order, for one `ncu --set full` capture (development tool), and summarises the
 capture into profiles/<round>/{ncu_full_summary.json,traffic.json}.
     ncu --set full --clock-control none --import-source on \
-        -k regex:"scan_smem|mapreduce_kernel|gevm_cols|gemv_kernel" -o /tmp/comp \
+        -k regex:"scan_lag|scan_smem|mapreduce_kernel|gevm_cols|gemv_kernel" -o /tmp/comp \
         python tools/ncu_components.py run
     ncu -i /tmp/comp.ncu-rep --page raw --csv > gpurun_out/comp_raw.csv
     python tools/ncu_components.py summarize gpurun_out/comp_raw.csv profiles/r02"""

@@ -19,6 +19,9 @@ sass = subprocess.run(["cuobjdump", "-sass", str(lib)], capture_output=True, tex
 funcs = re.split(r"\n\s+Function : ", sass)
 # family -> substring of the mangled name that picks one representative
 FAMILIES = {
+    "scan_lag_kernel (f32 sum)": ("scan_lag_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32ELb1"),
+    "scan_lag_kernel (affine, f64 carry)": ("scan_lag_kernel", "AffineOpELb1"),
+    "scan_lag_kernel (argmax, row-prefix ring)": ("scan_lag_kernel", "ArgMaxOpELb1"),
     "scan_smem_kernel (f32 sum, TMA tile)": ("scan_smem_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32ELb1"),
     "scan_smem_kernel (affine, f64 carry)": ("scan_smem_kernel", "AffineOpELb1"),
     "scan_smem_kernel (argmax)": ("scan_smem_kernel", "ArgMaxOpELb1"),
@@ -31,7 +34,7 @@ FAMILIES = {
     "reduce_ordered_kernel (f32 sum)": ("reduce_ordered_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32"),
 }
 KEYS = ["UTMALDG", "UTMASTG", "UBLKCP", "SYNCS", "LDG.E.NA.ENL2.256", "LDG.E.ENL2.256", "LDG", "STG", "LDS", "STS",
-        "IDP.4A", "ATOMG", "RED", "FENCE", "SHFL", "DFMA", "DMUL", "DADD", "FFMA", "FADD", "FMNMX", "MEMBAR", "CCTL"]
+        "IDP.4A", "ATOMG", "RED", "CCTL", "FENCE", "SHFL", "DFMA", "DMUL", "DADD", "FFMA", "FADD", "FMNMX", "MEMBAR", "ERRBAR"]
 summary = {}
 for fam, (kname, sub) in FAMILIES.items():
     cands = [f for f in funcs if f.split("\n", 1)[0].find(kname) >= 0 and sub in f.split("\n", 1)[0]]
