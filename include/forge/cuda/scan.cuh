@@ -749,7 +749,7 @@ struct LagArgs {
 };
 
 constexpr uint32_t kLagRing = 2048;  // row-prefix ring slots (> D + resident tickets)
-constexpr uint32_t kRingDiscard = 1, kRingBypass = 2;
+constexpr uint32_t kRingDiscard = 1, kRingBypass = 2, kRingDevNoWrite = 4;  // the last: FORGE_DEV probe only
 // Ring entry tag: the epoch and the lap of the slot (tile / R mod 4: a slot
 // holds lap L - 1, L or L + 1 of this launch, or older launches' entries),
 // complemented so a zeroed workspace never matches.
@@ -1045,7 +1045,7 @@ __global__ void __launch_bounds__(kScanThreads, 6)
           IO::write(L.tagg, k, IO::GW, epoch, kPartial, agg);  // compact: tile k at k * ST words
           if (tr) tr[uint64_t(k) * 8 + 3] = global_ns();
         });
-    if (kRing && threadIdx.x > 0)
+    if (kRing && threadIdx.x > 0 && !(L.ring_flags & kRingDevNoWrite))
       RingIO<A>::write(L.ring + (uint64_t(k % R) * kScanThreads + threadIdx.x) * RW, ring_tag(epoch, k, R),
                        row_ex.v);
     // the last tile of a group publishes the group aggregate (warp 1: it polls
