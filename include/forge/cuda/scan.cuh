@@ -1274,13 +1274,15 @@ inline bool scan_force_regs() {
   return v;
 }
 // Lag D of the lagged scan (scan_lag_kernel), in tiles; 0 = the single-pass
-// kernel.  Measured on B200 (148 SMs, f32 / i32 / affine / argmax at 2^28,
-// GB/s): D = 256: 4133 / 3744 / 3757 / 3401 (B waits for A's aggregates);
-// 448: 5368 / 5287 / 5038 / 4617; 512: 5290 / 5290 / 5112 / 4637; 768: 5184 /
-// 5185 / 4852 / 4427 (the re-read starts missing L2); single-pass kernel:
-// 4828 / 4849 / 4479 / 4517.  D scales with the resident tiles: 3.5 per SM.
+// kernel.  Measured on B200 (148 SMs, f32 / i32 / affine / argmax / Mat2 at
+// 2^28, GB/s, relaxed claims, row-prefix ring for argmax): D = 384: 4945 /
+// 4496 / 4385 / 4209 / 4305 (B waits for A's aggregates); 448: 5399 / 4923 /
+// 4841 / 4483 / 4852; 518: 5572 / 5344 / 5162 / 4915 / 5150; 600: 5600 / 5486
+// / 5246 / 4968 / 5266; 680: 5571 / 5497 / 5208 / 4972 / 5226; 760: 5484 /
+// 5397 / 5113 / 4950 / 5130; 1000: 4918 / 4895 / 4836 / 4679 / 4830 (the
+// re-read starts missing L2).  D scales with the resident tiles: 4 per SM.
 inline uint32_t scan_lag() {
-  static const uint32_t v = dev_knob("FORGE_SCAN_LAG", device_props().sm_count * 7 / 2);
+  static const uint32_t v = dev_knob("FORGE_SCAN_LAG", device_props().sm_count * 4);
   return v;
 }
 // kRingDiscard | kRingBypass (FORGE_DEV knob FORGE_SCAN_RING; kRingBypass is

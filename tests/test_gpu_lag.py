@@ -30,7 +30,7 @@ F = pytest.importorskip("paper_2603_18695_b200.forge")
 
 def lag_tiles():
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    return sms * 7 // 2
+    return sms * 4
 
 
 def threshold():

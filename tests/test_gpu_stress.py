@@ -88,7 +88,7 @@ def test_relaxed_protocol_mutant_is_caught(op, path):
         n = (1 << 22) + 17
     else:
         sms = torch.cuda.get_device_properties(0).multi_processor_count
-        n = (3 * (sms * 7 // 2) + 100) * (32768 // F.op_info(op)["t_size"]) + 17
+        n = (3 * (sms * 4) + 100) * (32768 // F.op_info(op)["t_size"]) + 17
     xs, want = [], []
     ws = dev.Workspace()
     # the two seeds differ above bit 40: element i of the generator depends on
