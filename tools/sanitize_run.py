@@ -27,6 +27,19 @@ for op in (capi.F32_SUM, capi.I32_MAX, capi.AFFINE_F32, capi.MAT2_U32, capi.UF8_
             if "commutative" not in str(e):
                 raise
         dev.reduce_ordered(op, x, n, out, ws)
+# the lagged scan: with the DEV library and FORGE_SCAN_LAG=16 it takes scans of
+# >= 128 full tiles (140 tiles + a tail here; argmax past the 2048-slot ring)
+if os.environ.get("FORGE_LIB") == "dev" and os.environ.get("FORGE_SCAN_LAG"):
+    from paper_2603_18695_b200.forge import op_info
+    for op, tiles in ((capi.F32_SUM, 140), (capi.ARGMAX_F32I32, 140), (capi.AFFINE_F32, 140),
+                      (capi.MAT2_U32, 140), (capi.ARGMAX_F32I32, 2100)):
+        n = tiles * (32768 // op_info(op)["t_size"]) + 17
+        x = dev.empty(op, n)
+        dev.fill_synthetic(op, x, n, 12)
+        y = dev.empty(op, n, "S")
+        for incl in (True, False):
+            dev.scan(op, incl, x, y, n, ws)
+        del x, y
 for op in (capi.MV_F32_PLUS_TIMES, capi.MV_F32_MIN_PLUS):
     for n, p in ((257, 129), (4096, 7), (64, 2048)):
         A = dev.empty(op, n * p)
