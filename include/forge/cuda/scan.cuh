@@ -515,26 +515,27 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
 
   const uint64_t t_start = a.trace ? global_ns() : 0;
   if (threadIdx.x == 0) {
-    // The tile to load is guessed as blockIdx.x and its TMA issued BEFORE the
-    // ticket round trip (CTAs are dispatched in index order in practice); the
-    // ticket stays the source of truth, so a mismatch only costs a reload.
+    // Tile blockIdx.x is prefetched into L2 BEFORE the ticket round trip; the
+    // ticket stays the source of truth, and the tile it names was prefetched
+    // by the CTA of that index, which started at about the same time (tickets
+    // match blockIdx.x for only 1-3 % of CTAs, but are close to it), so the
+    // shared-memory load after the claim is an L2 hit.  (A speculative
+    // shared-memory load of blockIdx.x had to land before the claimed tile
+    // could be loaded: 2^28 lagged f32 5.60 -> 5.88 TB/s with the prefetch.)
     const uint32_t g = blockIdx.x;
-    const bool gfull = uint64_t(g + 1) * kTile <= a.n;
     mbar_init(&bar, 1);
     fence_mbar_init();
-    if (gfull) load_tile(g);
+    if (uint64_t(g + 1) * kTile <= a.n) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        tma_prefetch_2d_hint(&tmap, 0, (int(g) * R + r) * kScanThreads, l2_policy_evict_normal());
+    }
     uint32_t e;
     const uint32_t t = claim_tile(a, e);
     s_tile = t;
     s_epoch = e;
     s_phase = 0;
-    if (t != g) {
-      if (gfull) mbar_wait(&bar, 0);  // drain the speculative copy
-      if (uint64_t(t + 1) * kTile <= a.n) {
-        load_tile(t);
-        s_phase = gfull ? 1u : 0u;
-      }
-    }
+    if (uint64_t(t + 1) * kTile <= a.n) load_tile(t);
   }
   __syncthreads();
   const uint64_t tile = s_tile;
@@ -749,7 +750,8 @@ struct LagArgs {
 };
 
 constexpr uint32_t kLagRing = 2048;  // row-prefix ring slots (> D + resident tickets)
-constexpr uint32_t kRingDiscard = 1, kRingBypass = 2, kRingDevNoWrite = 4;  // the last: FORGE_DEV probe only
+constexpr uint32_t kRingDiscard = 1, kRingBypass = 2;
+constexpr uint32_t kRingDevNoWrite = 4, kLagDevSpecSmem = 8;  // FORGE_DEV probes only
 // Ring entry tag: the epoch and the lap of the slot (tile / R mod 4: a slot
 // holds lap L - 1, L or L + 1 of this launch, or older launches' entries),
 // complemented so a zeroed workspace never matches.
@@ -836,15 +838,27 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   uint64_t* const tr = a.trace;  // FORGE_DEV builds: per-ticket phase stamps (tools/trace_lag.py)
   const uint64_t t_start = tr ? global_ns() : 0;
 
-  // ---- claim; the A load is issued speculatively for blockIdx.x first
+  // ---- claim.  Tile blockIdx.x is fetched into L2 while the claim is in
+  // flight: tickets follow CTA start order only roughly (97-99 % of CTAs get a
+  // ticket other than blockIdx.x, tools/trace_lag.py), but the tile a CTA
+  // claims was prefetched by the CTA with that index, which started at about
+  // the same time, so its shared-memory load right after the claim is an L2
+  // hit (or joins the fill in flight).  (A speculative shared-memory load of
+  // blockIdx.x instead had to land before the buffer could take the claimed
+  // tile: FORGE_DEV ring flag kLagDevSpecSmem.)
+  const bool spec_smem = (L.ring_flags & kLagDevSpecSmem) != 0;
   if (threadIdx.x == 0) {
     const uint32_t g = blockIdx.x;
     mbar_init(&bar, 1);
     fence_mbar_init();
     const uint64_t pol = l2_policy_evict_last();
     if (g < a.ntiles) {
-      mbar_arrive_expect_tx(&bar, kSmemTileBytes);
-      tma_load_2d_hint(buf, &tmap, 0, int(g) * kScanThreads, &bar, pol);
+      if (spec_smem) {
+        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+        tma_load_2d_hint(buf, &tmap, 0, int(g) * kScanThreads, &bar, pol);
+      } else {
+        tma_prefetch_2d_hint(&tmap, 0, int(g) * kScanThreads, pol);
+      }
     }
     uint64_t* word = reinterpret_cast<uint64_t*>(a.ctrl);
     // relaxed: nothing is ordered by the claim (every tile state carries its
@@ -859,8 +873,8 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     s_k = k;
     s_epoch = e;
     uint32_t ph = 0;  // parity of the barrier's next completion
-    if (k != g) {
-      if (g < a.ntiles) {
+    if (!spec_smem || k != g) {
+      if (spec_smem && g < a.ntiles) {
         mbar_wait(&bar, 0);  // drain the speculative copy
         ph = 1;
       }
