@@ -172,7 +172,9 @@ def kernel_of(kind, op):
     if kind == "mapreduce":
         return "mapreduce_kernel"
     if kind == "scan":
-        return "scan_lag_kernel"  # 2^28-element scans: the lagged kernel (scan.cuh)
+        # 2^28-element scans: the lagged kernel for 16-byte carries, the
+        # single-pass one otherwise (scan.cuh lag_scan_type_ok)
+        return "scan_lag_kernel" if op in (capi.AFFINE_F32, capi.MAT2_U32) else "scan_smem_kernel"
     if kind == "matvec":
         return "gevm_cols_kernel"
     return "gemv_kernel"

@@ -296,13 +296,6 @@ int forge_set_mutation_flags(int32_t relax_scan_flag, int32_t relax_mapreduce_fl
  * ablation above is never exercised.  seed = 0 turns it off. */
 int forge_set_schedule_perturbation(uint64_t seed, uint32_t delay_ns);
 
-/* Lagged scan (the default for large contiguous scans): bypass = 1 makes the
- * calling thread's subsequent scans ignore the row-prefix ring, so every tile
- * takes the fallback fold that normally runs only when a ring entry is stale.
- * TEST ONLY (results are bit-identical either way; tests/test_gpu_lag.py).
- * 0 restores the product path.  No reference counterpart (B200 kernel detail). */
-int forge_set_scan_ring_bypass(int32_t bypass);
-
 /* vload_pattern (intrinsics.hpp:190, intrinsics.cpp:29-33). segs has room for 16. */
 int forge_vload_pattern(uint64_t offset, uint32_t nitem, uint32_t* segs, uint32_t* count);
 

@@ -184,70 +184,6 @@ __device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
 __device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
-  uint64_t r;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
-  return r;
-}
-__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// Values written by other CTAs during the kernel, read at L2 (ld.global.cg:
-// never a stale L1 line) / written through to L2.
-template <class T>
-__device__ __forceinline__ T ld_l2(const T* p) {
-  static_assert(sizeof(T) == 4 || sizeof(T) == 8 || sizeof(T) == 16, "ld_l2: 4/8/16-byte values");
-  T v;
-  if constexpr (sizeof(T) == 4) {
-    const uint32_t w = __ldcg(reinterpret_cast<const unsigned int*>(p));
-    memcpy(&v, &w, 4);
-  } else if constexpr (sizeof(T) == 8) {
-    const uint2 w = __ldcg(reinterpret_cast<const uint2*>(p));
-    memcpy(&v, &w, 8);
-  } else {
-    const uint4 w = __ldcg(reinterpret_cast<const uint4*>(p));
-    memcpy(&v, &w, 16);
-  }
-  return v;
-}
-template <class T>
-__device__ __forceinline__ void st_l2(T* p, const T& v) {
-  static_assert(sizeof(T) == 4 || sizeof(T) == 8 || sizeof(T) == 16, "st_l2: 4/8/16-byte values");
-  if constexpr (sizeof(T) == 4) {
-    uint32_t w;
-    memcpy(&w, &v, 4);
-    __stcg(reinterpret_cast<unsigned int*>(p), w);
-  } else if constexpr (sizeof(T) == 8) {
-    uint2 w;
-    memcpy(&w, &v, 8);
-    __stcg(reinterpret_cast<uint2*>(p), w);
-  } else {
-    uint4 w;
-    memcpy(&w, &v, 16);
-    __stcg(reinterpret_cast<uint4*>(p), w);
-  }
-}
-// st_l2 with an L2 eviction-priority policy (createpolicy)
-template <class T>
-__device__ __forceinline__ void st_l2_hint(T* p, const T& v, uint64_t pol) {
-  static_assert(sizeof(T) == 4 || sizeof(T) == 8 || sizeof(T) == 16, "st_l2_hint: 4/8/16-byte values");
-  uint32_t w[4] = {0, 0, 0, 0};
-  memcpy(w, &v, sizeof(T));
-  if constexpr (sizeof(T) == 4)
-    asm volatile("st.global.cg.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(w[0]), "l"(pol) : "memory");
-  else if constexpr (sizeof(T) == 8)
-    asm volatile("st.global.cg.L2::cache_hint.v2.b32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(w[0]), "r"(w[1]), "l"(pol)
-                 : "memory");
-  else
-    asm volatile("st.global.cg.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(w[0]), "r"(w[1]),
-                 "r"(w[2]), "r"(w[3]), "l"(pol)
-                 : "memory");
-}
-// Drops a 128-byte L2 line without writing it back (its contents become
-// undefined): for scratch lines that are dead once read.
-__device__ __forceinline__ void discard_l2_line(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
 __device__ __forceinline__ void ld_relaxed_gpu_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];"
                : "=l"(a), "=l"(b)

@@ -169,7 +169,6 @@ struct ScanTestHooks {
   bool relax_epoch = false;
   uint64_t perturb_seed = 0;
   uint32_t perturb_ns = 0;
-  bool ring_bypass = false;  // lagged scan: B ignores the row-prefix ring and folds every tile itself
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -709,21 +708,10 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
 //             folds the group's 32 aggregates and publishes the group
 //             aggregate (group state kind PARTIAL).
 //   B(k - D)  the scan of tile j = k - D, D tiles behind: re-load it (an L2 hit:
-//             D tiles of reads + writes stay well inside the 126 MB L2),
-//             compose each row's exclusive prefix with the tile's, emit, TMA
+//             D tiles of reads + writes stay well inside the 126 MB L2), fold
+//             its rows, compose with the tile's exclusive prefix, emit, TMA
 //             store; the last tile of a group publishes the group's inclusive
 //             prefix (group state kind PREFIX).
-// Row prefixes: A(k) has every row's exclusive prefix inside the tile (its
-// block scan) and leaves them in a RING slot (slot k mod R, R = 2048 >> D plus
-// the spread of resident tickets); B(k - D) reads its row's prefix there
-// instead of folding the tile a second time (one pass over the tile in B, not
-// two).  No flags, no fences, no waits: every 32-bit chunk of an entry travels
-// in a 64-bit word {tag, chunk} (single-copy atomic, relaxed .gpu accesses),
-// tag = f(epoch, lap of the slot), so each thread validates its own entry; if
-// any entry of the tile is not A(j)'s (A(j) not yet visible, or already
-// overwritten by A(j + R)), the CTA folds the tile itself with A's exact code
-// (same tree, same bits).  B then drops the slot's dead lines from L2
-// (discard: no write-back of scratch that is never read again).
 // j's exclusive prefix needs only states published by LOWER tickets' A phases
 // (tile aggregates of j's group, group aggregates) plus, as a shortcut, group
 // PREFIXes of finished B phases: warp 0 reads them — one 32-lane round of
@@ -742,72 +730,12 @@ struct LagArgs {
   ScanArgs<T, S, F, Op> s;  // src, dst, f, op, identity, carry_in, total_out, ctrl, ntiles (full tiles)
   uint64_t* tagg;           // tile aggregates: STRIDE words per tile, compact
   uint64_t* gstate;         // group states: STRIDE words per group, compact
-  uint64_t* ring;           // ring slots: kScanThreads tagged row prefixes each
-  uint32_t ring_slots;      // R = min(ntiles, kLagRing)
-  uint32_t ring_flags;      // kRingDiscard | kRingBypass (test hook: B always folds)
+  uint32_t dev_flags;       // FORGE_DEV probes (kLagDevSpecSmem)
   uint32_t lag;             // D
   uint32_t nclaims;         // ntiles + D
 };
 
-constexpr uint32_t kLagRing = 2048;  // row-prefix ring slots (> D + resident tickets)
-constexpr uint32_t kRingDiscard = 1, kRingBypass = 2;
-constexpr uint32_t kRingDevNoWrite = 4, kLagDevSpecSmem = 8;  // FORGE_DEV probes only
-// Ring entry tag: the epoch and the lap of the slot (tile / R mod 4: a slot
-// holds lap L - 1, L or L + 1 of this launch, or older launches' entries),
-// complemented so a zeroed workspace never matches.
-__device__ __forceinline__ uint32_t ring_tag(uint32_t epoch, uint32_t tile, uint32_t slots) {
-  return ~(((epoch & 0x3fffffffu) << 2) | ((tile / slots) & 3u));
-}
-// Whether the lagged scan keeps the row-prefix ring (Op::kLagRowPrefixRing
-// overrides).  Measured on B200 at 2^28 (GB/s, ring vs B folding its tile):
-// argmax (8-byte A) 4,950 vs 4,500; f32 / i32 sums (4-byte A) 5,330 vs 5,320 /
-// 5,220 vs 5,240 (the fold is cheap); affine (16-byte f64 A: 8 KB of tagged
-// entries per tile) 4,490 vs 4,990 and Mat2 4,780 vs 4,960 (the ring's L2
-// footprint costs more re-read hits than the fold it saves).
-template <class Op, class = void>
-struct LagRingOverride {
-  static constexpr int value = -1;
-};
-template <class Op>
-struct LagRingOverride<Op, std::void_t<decltype(Op::kLagRowPrefixRing)>> {
-  static constexpr int value = Op::kLagRowPrefixRing ? 1 : 0;
-};
-template <class S, class Op>
-constexpr bool lag_ring() {
-  constexpr int o = LagRingOverride<Op>::value;
-  return o >= 0 ? o == 1 : sizeof(typename ScanMath<S, Op>::A) == 8;
-}
-
-template <class A>
-struct RingIO {
-  static constexpr int W = Words<A>::N;  // 64-bit words per entry
-  static_assert(W == 1 || W == 2 || W == 4, "ring entries of 4, 8 or 16 bytes");
-  static __device__ __forceinline__ void write(uint64_t* e, uint32_t tag, const A& v) {
-    const Words<A> w = to_words(v);
-    const uint64_t hi = uint64_t(tag) << 32;
-    if constexpr (W == 1) {
-      st_relaxed_gpu(e, hi | w.w[0]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < W; i += 2) st_relaxed_gpu_v2(e + i, hi | w.w[i], hi | w.w[i + 1]);
-    }
-  }
-  static __device__ __forceinline__ bool read(const uint64_t* e, uint32_t tag, A& v) {
-    uint64_t raw[W];
-    if constexpr (W == 1) raw[0] = ld_relaxed_gpu(e);
-    else if constexpr (W == 2) ld_relaxed_gpu_v2(e, raw[0], raw[1]);
-    else ld_relaxed_gpu_v4(e, raw[0], raw[1], raw[2], raw[3]);
-    bool ok = true;
-    Words<A> w;
-#pragma unroll
-    for (int i = 0; i < W; ++i) {
-      ok &= uint32_t(raw[i] >> 32) == tag;
-      w.w[i] = uint32_t(raw[i]);
-    }
-    v = from_words<A>(w);
-    return ok;
-  }
-};
+constexpr uint32_t kLagDevSpecSmem = 8;  // FORGE_DEV probe: speculative shared-memory load of blockIdx.x
 
 template <class T, class S, class F, class Op, bool Inclusive>
 __global__ void __launch_bounds__(kScanThreads, 6)
@@ -845,8 +773,8 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   // the same time, so its shared-memory load right after the claim is an L2
   // hit (or joins the fill in flight).  (A speculative shared-memory load of
   // blockIdx.x instead had to land before the buffer could take the claimed
-  // tile: FORGE_DEV ring flag kLagDevSpecSmem.)
-  const bool spec_smem = (L.ring_flags & kLagDevSpecSmem) != 0;
+  // tile: FORGE_DEV flag kLagDevSpecSmem.)
+  const bool spec_smem = (L.dev_flags & kLagDevSpecSmem) != 0;
   if (threadIdx.x == 0) {
     const uint32_t g = blockIdx.x;
     mbar_init(&bar, 1);
@@ -994,10 +922,10 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     if (tr && lane == 0) tr[uint64_t(k) * 8 + 4] = global_ns();
   }
 
-  constexpr bool kRing = lag_ring<S, Op>();
-  // The tile in `buf` folded: this row's exclusive prefix inside the tile,
-  // (warps before) o (lanes before); s_warp[NW - 1] = the tile aggregate.
-  // A(k) and B's fallback run exactly this code, so both give the same bits.
+  // The tile in `buf` folded and block-scanned (A: its aggregate, passed to
+  // on_aggregate by warp 0 lane NW-1; B: also this row's exclusive prefix
+  // inside the tile, (warps before) o (lanes before)).  A and B run the same
+  // tree, so A's published aggregate and B's PREFIX are the same bits.
   auto tile_row_prefix = [&](auto want_row, auto sync_first, auto&& on_aggregate) -> Opt<A> {
     Opt<A> tot;
     auto fold_chunk = [&](int c) {
@@ -1040,16 +968,13 @@ __global__ void __launch_bounds__(kScanThreads, 6)
       return Opt<A>{A{}, false};
     }
   };
-  const uint32_t R = L.ring_slots;
-  constexpr int RW = RingIO<A>::W;
 
-  // ---- A: fold tile k, publish its aggregate, leave its row prefixes in the ring
+  // ---- A: fold tile k, publish its aggregate
   if (hasA) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
     if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 2] = global_ns();
-    const Opt<A> row_ex =
-        tile_row_prefix(std::bool_constant<kRing>{}, std::false_type{}, [&](const A& total) {
+    tile_row_prefix(std::false_type{}, std::false_type{}, [&](const A& total) {
           const C agg = M::to_c(total);
           s_carry_agg = agg;
           if (a.perturb_ns && ((uint64_t(k) * 0x9E3779B97F4A7C15ull) ^ a.perturb_seed) % 8 == 0) {  // test hook
@@ -1059,9 +984,6 @@ __global__ void __launch_bounds__(kScanThreads, 6)
           IO::write(L.tagg, k, IO::GW, epoch, kPartial, agg);  // compact: tile k at k * ST words
           if (tr) tr[uint64_t(k) * 8 + 3] = global_ns();
         });
-    if (kRing && threadIdx.x > 0 && !(L.ring_flags & kRingDevNoWrite))
-      RingIO<A>::write(L.ring + (uint64_t(k % R) * kScanThreads + threadIdx.x) * RW, ring_tag(epoch, k, R),
-                       row_ex.v);
     // the last tile of a group publishes the group aggregate (warp 1: it polls
     // the group's other 31 aggregates, published by lower tickets)
     if (k % kLagGroup == kLagGroup - 1 && warp == 1) {
@@ -1094,26 +1016,15 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   __syncthreads();  // every read of A's tile is done (and s_carry / s_self_agg are visible)
   if (!hasB) return;
 
-  // ---- B: re-load tile j (L2) and its row prefixes (ring), emit, store
+  // ---- B: re-load tile j (L2), fold it, compose with the carry, emit, store
   if (threadIdx.x == 0) {
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&bar, kSmemTileBytes);
     tma_load_2d_hint(buf, &tmap, 0, int(j) * kScanThreads, &bar, l2_policy_evict_first());
   }
-  const uint64_t* const slot = L.ring + uint64_t(uint32_t(j) % R) * kScanThreads * RW;
-  Opt<A> row_ex{A{}, threadIdx.x > 0};
-  bool ring_ok = kRing && !(L.ring_flags & kRingBypass);
-  if (ring_ok && threadIdx.x > 0)
-    ring_ok = RingIO<A>::read(slot + threadIdx.x * RW, ring_tag(epoch, uint32_t(j), R), row_ex.v);
   mbar_wait(&bar, phase);
   if (tr && threadIdx.x == 0) tr[uint64_t(k) * 8 + 5] = global_ns();
-  // an entry that is not A(j)'s (not yet visible, or already overwritten by
-  // A(j + R)), or no ring: the CTA folds the tile itself
-  if constexpr (kRing) {
-    if (!__syncthreads_and(ring_ok)) row_ex = tile_row_prefix(std::true_type{}, std::true_type{}, [](const A&) {});
-  } else {
-    row_ex = tile_row_prefix(std::true_type{}, std::true_type{}, [](const A&) {});
-  }
+  const Opt<A> row_ex = tile_row_prefix(std::true_type{}, std::true_type{}, [](const A&) {});
   const Opt<C> carry = s_carry;
   if (threadIdx.x == 0 && (j % kLagGroup == kLagGroup - 1 || j == a.ntiles - 1)) {
     const C agg = s_self_agg;  // tile j's aggregate (A(j)'s, read by the look-back)
@@ -1182,21 +1093,15 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   else
     emit_rows(std::false_type{});
   fence_proxy_async_smem();
-  __syncthreads();  // every row prefix of the slot has been read and used
+  __syncthreads();
   if (threadIdx.x == 0) {
     if (tr) tr[uint64_t(k) * 8 + 6] = global_ns();
     tma_store_2d_hint(&tmap_out, 0, int(j) * kScanThreads, buf, l2_policy_evict_first());
     tma_store_commit();
     tma_store_wait_read();
     if (tr) tr[uint64_t(k) * 8 + 7] = global_ns();
-  } else if (kRing && warp == 1 && (L.ring_flags & kRingDiscard)) {
-    // the slot's lines are dead (read once): drop them from L2 without a
-    // write-back.  A hint only — an entry lost to a late discard reads as
-    // not-A(j)'s and its tile is folded by B.
-    constexpr uint32_t kSlotLines = uint32_t(kScanThreads * RW * 8) / 128u;
-#pragma unroll
-    for (uint32_t i = lane; i < kSlotLines; i += kWarp) discard_l2_line(reinterpret_cast<const char*>(slot) + i * 128u);
   }
+
 }
 
 
@@ -1244,8 +1149,7 @@ struct ScanWs {
 #define FORGE_SCAN_LAG_MAX_T 16  // largest element (bytes) taken by the lagged scan
 #endif
 
-// Lagged-scan workspace: [256-byte control block | ring slots (min(tiles,
-// kLagRing) x 256 tagged row prefixes) | tile
+// Lagged-scan workspace: [256-byte control block | tile
 // aggregates | group states | full-tile total | tail sub-workspace].
 template <class T, class S, class Op>
 struct LagWs {
@@ -1253,11 +1157,7 @@ struct LagWs {
   using A = typename ScanMath<S, Op>::A;
   static constexpr uint64_t ST = uint64_t(TileStateIO<C>::STRIDE);
   static constexpr uint64_t align(uint64_t v) { return (v + 255) & ~uint64_t(255); }
-  static uint64_t ring_slots(uint64_t tiles) { return tiles < kLagRing ? tiles : kLagRing; }
-  static constexpr uint64_t kSlotBytes =  // tagged entries
-      lag_ring<S, Op>() ? uint64_t(kScanThreads) * RingIO<A>::W * 8 : 0;
-  static uint64_t ring_off() { return 256; }
-  static uint64_t tagg_off(uint64_t tiles) { return ring_off() + align(ring_slots(tiles) * kSlotBytes); }
+  static uint64_t tagg_off(uint64_t) { return 256; }
   static uint64_t gstate_off(uint64_t tiles) { return tagg_off(tiles) + align(tiles * ST * 8); }
   static uint64_t total_off(uint64_t tiles) { return gstate_off(tiles) + align(ceil_div(tiles, kLagGroup) * ST * 8); }
   static uint64_t tail_off(uint64_t tiles) { return total_off(tiles) + 256; }
@@ -1267,10 +1167,17 @@ struct LagWs {
   }
 };
 
+// The lagged kernel takes 16-byte carries (f64 affine, Mat2); for carries of
+// at most 8 bytes the single-pass kernel is as fast or faster since the claim
+// became relaxed and the tile an L2 prefetch (2^28 / 2^27, GB/s, single-pass
+// vs lagged): f32 sum 5,870 / 5,900, f64 sum 5,727 / 5,690, i32 sum 5,933 /
+// 5,818, i32 max 5,951 / 5,790, i64 sum 5,888 / 5,689, argmax 5,490 / 5,424
+// (with the row-prefix ring), affine 5,414 / 5,605, Mat2 5,419 /
+// 5,606.  32-byte carries (quaternion) spill at 6 CTAs/SM.
 template <class T, class S, class Op>
 constexpr bool lag_scan_type_ok() {
   return smem_scan_type_ok<T>() && sizeof(S) == sizeof(T) && sizeof(T) <= FORGE_SCAN_LAG_MAX_T &&
-         sizeof(typename CarryTraits<S, Op>::C) <= 16;
+         sizeof(typename CarryTraits<S, Op>::C) > 8 && sizeof(typename CarryTraits<S, Op>::C) <= 16;
 }
 
 
@@ -1289,7 +1196,8 @@ inline bool scan_force_regs() {
 }
 // Lag D of the lagged scan (scan_lag_kernel), in tiles; 0 = the single-pass
 // kernel.  Measured on B200 (148 SMs, f32 / i32 / affine / argmax / Mat2 at
-// 2^28, GB/s, relaxed claims, row-prefix ring for argmax): D = 384: 4945 /
+// 2^28, GB/s, relaxed claims, row-prefix ring for argmax — all five took the
+// lagged kernel then): D = 384: 4945 /
 // 4496 / 4385 / 4209 / 4305 (B waits for A's aggregates); 448: 5399 / 4923 /
 // 4841 / 4483 / 4852; 518: 5572 / 5344 / 5162 / 4915 / 5150; 600: 5600 / 5486
 // / 5246 / 4968 / 5266; 680: 5571 / 5497 / 5208 / 4972 / 5226; 760: 5484 /
@@ -1299,10 +1207,9 @@ inline uint32_t scan_lag() {
   static const uint32_t v = dev_knob("FORGE_SCAN_LAG", device_props().sm_count * 4);
   return v;
 }
-// kRingDiscard | kRingBypass (FORGE_DEV knob FORGE_SCAN_RING; kRingBypass is
-// also the test hook ScanTestHooks::ring_bypass)
-inline uint32_t scan_ring_flags() {
-  static const uint32_t v = dev_knob("FORGE_SCAN_RING", kRingDiscard);
+// FORGE_DEV knob FORGE_SCAN_LAG_FLAGS (kLagDevSpecSmem)
+inline uint32_t scan_lag_dev_flags() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_LAG_FLAGS", 0);
   return v;
 }
 inline bool scan_no_tma_store() {
@@ -1403,8 +1310,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
-  // lagged scan: elements and carries of at most 16 bytes (a 32-byte f64
-  // quaternion carry spills at 6 CTAs/SM: 3.20 TB/s lagged vs 3.57 single-pass)
+  // lagged scan: 16-byte carries (lag_scan_type_ok)
   if constexpr (lag_scan_type_ok<T, S, Op>()) {
     if (const uint32_t lag = scan_lag(); lag && src_stride == 1 && dst_stride == 1) {
       constexpr uint64_t kTile = uint64_t(kScanThreads) * smem_scan_items<T>();
@@ -1420,9 +1326,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
         LagArgs<T, S, F, Op> L{a,
                                reinterpret_cast<uint64_t*>(w + LW::tagg_off(nfull)),
                                reinterpret_cast<uint64_t*>(w + LW::gstate_off(nfull)),
-                               reinterpret_cast<uint64_t*>(w + LW::ring_off()),
-                               uint32_t(LW::ring_slots(nfull)),
-                               scan_ring_flags() | (hooks.ring_bypass ? kRingBypass : 0u),
+                               scan_lag_dev_flags(),
                                lag,
                                uint32_t(nfull + lag)};
         L.s.ntiles = uint32_t(nfull);

@@ -297,8 +297,7 @@ inline uint64_t b200_scan_ws_bytes(uint64_t n, uint32_t accum_size) {
     const uint64_t tiles = n / tile;
     if (tiles >= std::max<uint64_t>(3 * (b200_sm_count() * 4), 128)) {  // cuda::lag_min_tiles()
       const uint64_t smb = b200_state_min_bytes(accum_size);
-      lag = 256 + rup(std::min<uint64_t>(tiles, 2048) * 256 * 4 * accum_size, 256) +  // tagged entries
-            rup(tiles * smb, 256) + rup((tiles + 31) / 32 * smb, 256) + 256 +
+      lag = 256 + rup(tiles * smb, 256) + rup((tiles + 31) / 32 * smb, 256) + 256 +
             b200_scan_ws_base(tile, accum_size);
     }
   }

@@ -134,7 +134,6 @@ _SIGNATURES = {
     "forge_vcopy": (C.c_int, [_P, View, View, _u32, C.POINTER(ArchParams), C.POINTER(LaunchReport)]),
     "forge_set_mutation_flags": (C.c_int, [_i32, _i32]),
     "forge_set_schedule_perturbation": (C.c_int, [_u64, _u32]),
-    "forge_set_scan_ring_bypass": (C.c_int, [C.c_int32]),
     "forge_vload_pattern": (C.c_int, [_u64, _u32, C.POINTER(_u32), C.POINTER(_u32)]),
     "forge_dev_workspace_bytes": (C.c_int, [C.c_int, C.c_int, _u64, _u64, C.POINTER(_u64)]),
     "forge_dev_mapreduce": (C.c_int, [C.c_int, _P, _u64, _P, _P, _u64, _P]),

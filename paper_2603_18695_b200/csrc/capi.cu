@@ -337,11 +337,6 @@ int forge_set_schedule_perturbation(uint64_t seed, uint32_t delay_ns) {
   return FORGE_OK;
 }
 
-int forge_set_scan_ring_bypass(int32_t bypass) {
-  g_ring_bypass = bypass != 0;
-  return FORGE_OK;
-}
-
 
 
 

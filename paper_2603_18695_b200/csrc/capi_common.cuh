@@ -25,10 +25,9 @@ inline thread_local std::string g_last_error;
 inline thread_local prim::MutationFlags g_mutate;  // forge_set_mutation_flags (test-only ablation)
 inline thread_local uint64_t g_perturb_seed = 0;   // forge_set_schedule_perturbation (test only)
 inline thread_local uint32_t g_perturb_ns = 0;
-inline thread_local bool g_ring_bypass = false;  // forge_set_scan_ring_bypass (test only)
 
 inline cuda::ScanTestHooks scan_hooks() {
-  return cuda::ScanTestHooks{g_mutate.relax_scan_flag, g_perturb_seed, g_perturb_ns, g_ring_bypass};
+  return cuda::ScanTestHooks{g_mutate.relax_scan_flag, g_perturb_seed, g_perturb_ns};
 }
 
 inline void set_error(const std::string& s) { g_last_error = s; }

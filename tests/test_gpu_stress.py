@@ -80,9 +80,10 @@ def test_relaxed_protocol_mutant_is_caught(op, path):
     # seeded schedules.  Two inputs alternate on one workspace; every output is
     # checked bit for bit.  The product protocol must pass under the same
     # schedule, the mutant must be caught.
-    # path "lagged": above the lagged scan's threshold (3 lags of 3.5 tiles per
-    # SM, include/forge/cuda/scan.cuh), whose A phases publish the aggregates
-    # the mutant may confuse with the previous launch's
+    # path "lagged": above the lagged scan's threshold (3 lags of 4 tiles per
+    # SM, include/forge/cuda/scan.cuh), where Mat2 (16-byte carry) takes the
+    # lagged kernel, whose A phases publish the aggregates the mutant may
+    # confuse with the previous launch's (i32 / f32: the single-pass kernel)
     lib = capi.load()
     if path == "single_pass":
         n = (1 << 22) + 17

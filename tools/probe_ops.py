@@ -1,4 +1,5 @@
-"""Lagged scan with / without the row-prefix ring (forge_set_scan_ring_bypass), 2^28 (development)."""
+"""Scan GB/s of every lag-eligible menu op at 2^28 (2^27 for 16-byte elements) (development).
+FORGE_LIB=dev FORGE_SCAN_LAG=0 selects the single-pass kernel."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,20 +17,20 @@ def t(fn, reps=10):
     x = sorted(a.elapsed_time(b) for a, b in ev); return x[len(x) // 2]
 
 
-lib = capi.load()
 ws = dev.Workspace()
 out = {}
-for name, op in (("i64", capi.I64_SUM), ("f64", capi.F64_SUM), ("argmax", capi.ARGMAX_F32I32),
-                 ("f32", capi.F32_SUM), ("affine", capi.AFFINE_F32), ("mat2", capi.MAT2_U32)):
+for name in ("F32_SUM", "F32_SUMSQ", "F32_MAX", "F64_SUM", "I32_SUM", "I32_MAX", "U32_SUM", "I64_SUM",
+             "AFFINE_F32", "ARGMAX_F32I32", "MAT2_U32", "LSE_F32", "QUAT_F32"):
+    op = getattr(capi, name, None)
+    if op is None:
+        continue
     inf = op_info(op)
     n = 1 << 28 if inf["t_size"] <= 8 else 1 << 27
     src = dev.empty(op, n); dev.fill_synthetic(op, src, n, 3); dst = dev.empty(op, n, "S")
-    r = {}
-    for byp in (0, 1, 0):
-        lib.forge_set_scan_ring_bypass(byp)
+    try:
         ms = t(lambda: dev.scan(op, True, src, dst, n, ws))
-        r[f"bypass{byp}"] = round(n * (inf["t_size"] + inf["s_size"]) / ms / 1e6, 1)
-    lib.forge_set_scan_ring_bypass(0)
-    out[name] = r
+        out[name] = round(n * (inf["t_size"] + inf["s_size"]) / ms / 1e6, 1)
+    except Exception as e:
+        out[name] = str(e)[:60]
     del src, dst
-print(json.dumps(out))
+print(json.dumps({"lag": os.environ.get("FORGE_SCAN_LAG", "default"), "gbs": out}))

@@ -9,7 +9,7 @@ from paper_2603_18695_b200 import capi, dev  # noqa: E402
 
 op = capi.F32_SUM
 out = {}
-for lg in (18, 20, 21, 22, 23, 24, 26):
+for lg in (18, 20, 21, 22, 23, 24, 25, 26, 27):
     n = 1 << lg
     src = dev.empty(op, n)
     dev.fill_synthetic(op, src, n, 1)
