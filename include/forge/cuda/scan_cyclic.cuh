@@ -102,6 +102,12 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
+    {  // L2 prefetch of ticket blockIdx.x's tile while the claim is in flight (scan.cuh)
+      const uint32_t gv = blockIdx.x % a.nvirt;
+      const uint64_t gl = blockIdx.x / a.nvirt;
+      if (gl < a.local_tiles[gv] && (gl + 1) * kTile <= a.local_n[gv])
+        tma_prefetch_2d_hint(&maps.in[gv], 0, int(gl) * kScanThreads, l2_policy_evict_normal());
+    }
     const uint32_t q = atom_add_relaxed_gpu(a.ctrl, 1u);  // orders nothing (states carry the epoch)
     if (q == a.nclaims - 1) st_relaxed_gpu(a.ctrl, 0u);
     s_q = q;
