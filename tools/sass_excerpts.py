@@ -19,9 +19,8 @@ sass = subprocess.run(["cuobjdump", "-sass", str(lib)], capture_output=True, tex
 funcs = re.split(r"\n\s+Function : ", sass)
 # family -> substring of the mangled name that picks one representative
 FAMILIES = {
-    "scan_lag_kernel (f32 sum)": ("scan_lag_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32ELb1"),
     "scan_lag_kernel (affine, f64 carry)": ("scan_lag_kernel", "AffineOpELb1"),
-    "scan_lag_kernel (argmax, row-prefix ring)": ("scan_lag_kernel", "ArgMaxOpELb1"),
+    "scan_lag_kernel (Mat2, 16-byte carry)": ("scan_lag_kernel", "Mat2MulELb1"),
     "scan_smem_kernel (f32 sum, TMA tile)": ("scan_smem_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32ELb1"),
     "scan_smem_kernel (affine, f64 carry)": ("scan_smem_kernel", "AffineOpELb1"),
     "scan_smem_kernel (argmax)": ("scan_smem_kernel", "ArgMaxOpELb1"),
@@ -33,7 +32,7 @@ FAMILIES = {
     "vcopy_kernel": ("vcopy_kernel", ""),
     "reduce_ordered_kernel (f32 sum)": ("reduce_ordered_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32"),
 }
-KEYS = ["UTMALDG", "UTMASTG", "UBLKCP", "SYNCS", "LDG.E.NA.ENL2.256", "LDG.E.ENL2.256", "LDG", "STG", "LDS", "STS",
+KEYS = ["UTMALDG", "UTMASTG", "UTMAPF", "UBLKCP", "SYNCS", "LDG.E.NA.ENL2.256", "LDG.E.ENL2.256", "LDG", "STG", "LDS", "STS",
         "IDP.4A", "ATOMG", "RED", "CCTL", "FENCE", "SHFL", "DFMA", "DMUL", "DADD", "FFMA", "FADD", "FMNMX", "MEMBAR", "ERRBAR"]
 summary = {}
 for fam, (kname, sub) in FAMILIES.items():
