@@ -151,6 +151,7 @@ struct ScanArgs {
                           // primitives.hpp:64-67): stale states of earlier launches are accepted
   uint64_t perturb_seed;  // test schedule perturbation (ScanTestHooks), 0 = off
   uint32_t perturb_ns;
+  uint32_t prefetch_ahead;  // CTA g L2-prefetches tile g + prefetch_ahead (0: tile g; scan_prefetch_ahead)
 };
 
 // Test-only hooks of one scan launch (both off in production):
@@ -524,11 +525,14 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
     const uint32_t g = blockIdx.x;
     mbar_init(&bar, 1);
     fence_mbar_init();
-    if (uint64_t(g + 1) * kTile <= a.n) {
+    const uint64_t gp = uint64_t(g) + a.prefetch_ahead;
+    auto prefetch = [&](uint64_t t) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        tma_prefetch_2d_hint(&tmap, 0, (int(g) * R + r) * kScanThreads, l2_policy_evict_normal());
-    }
+        tma_prefetch_2d_hint(&tmap, 0, (int(t) * R + r) * kScanThreads, l2_policy_evict_normal());
+    };
+    if (a.prefetch_ahead && g < a.prefetch_ahead && uint64_t(g + 1) * kTile <= a.n) prefetch(g);
+    if ((gp + 1) * kTile <= a.n) prefetch(gp);
     uint32_t e;
     const uint32_t t = claim_tile(a, e);
     s_tile = t;
@@ -784,10 +788,12 @@ __global__ void __launch_bounds__(kScanThreads, 6)
       if (spec_smem) {
         mbar_arrive_expect_tx(&bar, kSmemTileBytes);
         tma_load_2d_hint(buf, &tmap, 0, int(g) * kScanThreads, &bar, pol);
-      } else {
+      } else if (!a.prefetch_ahead || g < a.prefetch_ahead) {
         tma_prefetch_2d_hint(&tmap, 0, int(g) * kScanThreads, pol);
       }
     }
+    if (!spec_smem && a.prefetch_ahead && uint64_t(g) + a.prefetch_ahead < a.ntiles)
+      tma_prefetch_2d_hint(&tmap, 0, int(g + a.prefetch_ahead) * kScanThreads, pol);
     uint64_t* word = reinterpret_cast<uint64_t*>(a.ctrl);
     // relaxed: nothing is ordered by the claim (every tile state carries its
     // launch's epoch; the workspace memset precedes the launch).  An acq_rel
@@ -1212,6 +1218,19 @@ inline uint32_t scan_lag_dev_flags() {
   static const uint32_t v = dev_knob("FORGE_SCAN_LAG_FLAGS", 0);
   return v;
 }
+// L2 prefetch distance of the single-pass tile kernel, in tiles: CTA g
+// prefetches tile g + ahead, so the tile a CTA claims is in L2 before the
+// claim returns.  Measured (2^28, GB/s, f32 / i32 / argmax): ahead 0 (the
+// CTA's own tile): 5,880 / 5,950 / 5,472; 100: 6,054 / 6,161 / 5,574; 200:
+// 6,054-6,089 / 6,161 / 5,574; 300: 6,054-6,089 / 6,160 / 5,574; 600: 5,823 /
+// 5,883 / 5,516; 900: 4,850 / 4,850 / 5,045 (the prefetched tiles start to be
+// evicted before use) — one tile per SM.  The lagged kernel keeps 0 (its L2
+// already holds the D-tile re-read window: affine 5,620 at 0 and 100, 5,575
+// at 300, 4,950 at 600).
+inline uint32_t scan_prefetch_ahead() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_PREFETCH_AHEAD", device_props().sm_count);
+  return v;
+}
 inline bool scan_no_tma_store() {
   static const bool v = dev_knob("FORGE_SCAN_NO_TMA_STORE", 0) != 0;
   return v;
@@ -1306,7 +1325,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
                           static_cast<uint32_t*>(ws), 0u, 0u, scan_lookback_mode(), nullptr,
                           scan_backoff_ns(), hooks.relax_epoch ? 0u : 0x3fffffffu, hooks.perturb_seed,
-                          hooks.perturb_ns};
+                          hooks.perturb_ns, scan_prefetch_ahead()};
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
@@ -1330,6 +1349,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                                lag,
                                uint32_t(nfull + lag)};
         L.s.ntiles = uint32_t(nfull);
+        L.s.prefetch_ahead = 0;  // scan_prefetch_ahead
 #ifdef FORGE_DEV
         L.s.trace = scan_trace_for(nfull + lag);
 #endif
