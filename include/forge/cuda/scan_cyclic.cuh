@@ -60,6 +60,7 @@ struct CyclicArgs {
   uint32_t rank0, nvirt;                // virtual shard v of this launch is rank rank0 + v
   uint32_t nclaims;                     // sum of local_tiles over this launch's virtual shards
   uint32_t stride;                      // 64-bit words per tile state slot
+  uint32_t prefetch_ahead;              // CTA g L2-prefetches ticket g + this's tile (launch_scan_cyclic)
   F f;
   Op op;
   S identity;
@@ -102,12 +103,17 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-    {  // L2 prefetch of ticket blockIdx.x's tile while the claim is in flight (scan.cuh)
-      const uint32_t gv = blockIdx.x % a.nvirt;
-      const uint64_t gl = blockIdx.x / a.nvirt;
+    // L2 prefetch of ticket blockIdx.x + ahead's tile while the claim is in
+    // flight (scan.cuh scan_prefetch_ahead); the first `ahead` CTAs also
+    // prefetch their own guessed tile
+    auto prefetch = [&](uint64_t q) {
+      const uint32_t gv = uint32_t(q % a.nvirt);
+      const uint64_t gl = q / a.nvirt;
       if (gl < a.local_tiles[gv] && (gl + 1) * kTile <= a.local_n[gv])
         tma_prefetch_2d_hint(&maps.in[gv], 0, int(gl) * kScanThreads, l2_policy_evict_normal());
-    }
+    };
+    if (blockIdx.x < a.prefetch_ahead || a.prefetch_ahead == 0) prefetch(blockIdx.x);
+    if (a.prefetch_ahead) prefetch(uint64_t(blockIdx.x) + a.prefetch_ahead);
     const uint32_t q = atom_add_relaxed_gpu(a.ctrl, 1u);  // orders nothing (states carry the epoch)
     if (q == a.nclaims - 1) st_relaxed_gpu(a.ctrl, 0u);
     s_q = q;
@@ -332,6 +338,7 @@ cudaError_t launch_scan_cyclic(CyclicArgs<T, S, F, Op> a, bool inclusive, cudaSt
   if (claims == 0) return cudaSuccess;
   a.nclaims = claims;
   a.stride = cyclic_stride<S, Op>();
+  a.prefetch_ahead = scan_prefetch_ahead();
   auto k1 = scan_cyclic_kernel<T, S, F, Op, true>;
   auto k0 = scan_cyclic_kernel<T, S, F, Op, false>;
   static thread_local int done_dev = -1;
