@@ -258,6 +258,19 @@ def cpu_composite(reps: int = 7, with_c1: bool = True) -> dict:
             continue
         tot_bytes += byts
         tot_med += med
+    if with_c1 and kind_of == "reference":
+        # the reference's deterministic single-core backend (Backend::Simulator,
+        # SURVEY.md §8(d)) on C1 as well: wall clock around the call
+        x = orc.fill(0, CPU_C1, 0x5EED0C01)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            orc.ref_scan(0, True, x, backend=orc.SIM)
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        per["C1_scan_f32_sum_incl_2^20_simulator"] = {
+            "gbs": CPU_C1 * 8 / ts[2] / 1e9, "median_s": ts[2], "min_s": ts[0], "runs": 5, "bytes": CPU_C1 * 8,
+            "n": CPU_C1, "note": "reference VM Backend::Simulator (1 core, deterministic schedule); beside, not in value"}
     nproc = os.cpu_count() or 1
     workers = min(max(nproc, 2), 16)
     return {"value": tot_bytes / tot_med / 1e9, "unit": "GB/s",
