@@ -299,6 +299,22 @@ int forge_set_schedule_perturbation(uint64_t seed, uint32_t delay_ns);
 /* vload_pattern (intrinsics.hpp:190, intrinsics.cpp:29-33). segs has room for 16. */
 int forge_vload_pattern(uint64_t offset, uint32_t nitem, uint32_t* segs, uint32_t* count);
 
+/* Ordering litmus tests (forge::lit, include/forge/litmus.hpp; reference
+ * proj/include/forge/litmus.hpp, proj/src/litmus.cpp:169-350).  The text format
+ * of parse_litmus ("blocks=<n> cells=<k>", "B<i>: st|ld <cell> [rel|acq|rlx]
+ * [=<imm>]", "assert <expr>").  forge_litmus_parse only validates (no device
+ * needed; FORGE_ERR_PARSE_ERROR with the message in forge_last_error()).
+ * forge_litmus_run executes instances seed_begin .. seed_end-1 on the GPU (each
+ * block of the program a CTA on its own SM) and fills `out`; `histogram` (may
+ * be NULL) receives "<count>\t<outcome>\n" lines, most frequent first, cut
+ * at histogram_cap bytes (always NUL-terminated when histogram_cap > 0). */
+typedef struct forge_litmus_result {
+  uint64_t seeds_run, assert_violations, faults, distinct_outcomes;
+} forge_litmus_result;
+int forge_litmus_parse(const char* spec_text);
+int forge_litmus_run(const char* spec_text, uint64_t seed_begin, uint64_t seed_end, forge_litmus_result* out,
+                     char* histogram, uint64_t histogram_cap);
+
 /* ---------------------------------------------------------------------------
  * Device-pointer layer: stream-ordered, asynchronous, no host synchronisation.
  * `stream` is a cudaStream_t (NULL = the legacy default stream).  `ws` is caller

@@ -95,6 +95,12 @@ class LaunchReport(C.Structure):
 # name -> (restype, argtypes); exactly the declarations of include/forge.h
 _P = C.c_void_p
 _u32, _u64, _i32 = C.c_uint32, C.c_uint64, C.c_int32
+class LitmusResult(C.Structure):
+    """forge_litmus_result (include/forge.h)."""
+    _fields_ = [("seeds_run", C.c_uint64), ("assert_violations", C.c_uint64), ("faults", C.c_uint64),
+                ("distinct_outcomes", C.c_uint64)]
+
+
 _SIGNATURES = {
     "forge_last_error": (C.c_char_p, []),
     "forge_abi_version": (C.c_int, []),
@@ -135,6 +141,8 @@ _SIGNATURES = {
     "forge_set_mutation_flags": (C.c_int, [_i32, _i32]),
     "forge_set_schedule_perturbation": (C.c_int, [_u64, _u32]),
     "forge_vload_pattern": (C.c_int, [_u64, _u32, C.POINTER(_u32), C.POINTER(_u32)]),
+    "forge_litmus_parse": (C.c_int, [C.c_char_p]),
+    "forge_litmus_run": (C.c_int, [C.c_char_p, _u64, _u64, C.POINTER(LitmusResult), C.c_char_p, _u64]),
     "forge_dev_workspace_bytes": (C.c_int, [C.c_int, C.c_int, _u64, _u64, C.POINTER(_u64)]),
     "forge_dev_mapreduce": (C.c_int, [C.c_int, _P, _u64, _P, _P, _u64, _P]),
     "forge_dev_reduce_ordered": (C.c_int, [C.c_int, _P, _u64, _P, _P, _u64, _P]),

@@ -3,6 +3,7 @@
 // points live in capi_scan.cu, capi_reduce.cu and capi_matrix.cu so the
 // menu's kernel instantiations compile in parallel.
 #include "capi_common.cuh"
+#include "forge/litmus.hpp"
 
 // ---------------------------------------------------------------------------
 // Synthetic data on the device (bit-identical to oracle/oracle.c gen_one).
@@ -402,6 +403,44 @@ int forge_vload_pattern(uint64_t offset, uint32_t nitem, uint32_t* segs, uint32_
     intr::LoadPattern p = intr::vload_pattern(offset, nitem);
     for (uint32_t i = 0; i < p.count; ++i) segs[i] = p.seg[i];
     *count = p.count;
+    return FORGE_OK;
+  });
+}
+
+// ---- litmus (forge::lit) -------------------------------------------------------
+
+int forge_litmus_parse(const char* spec_text) {
+  return guarded([&]() -> int {
+    if (!spec_text) raise(ErrorCode::InvalidArgument, "litmus: null text");
+    (void)lit::parse_litmus(spec_text);
+    return FORGE_OK;
+  });
+}
+
+int forge_litmus_run(const char* spec_text, uint64_t seed_begin, uint64_t seed_end, forge_litmus_result* out,
+                     char* histogram, uint64_t histogram_cap) {
+  return guarded([&]() -> int {
+    if (!spec_text || !out) raise(ErrorCode::InvalidArgument, "litmus: null argument");
+    const lit::LitmusSpec spec = lit::parse_litmus(spec_text);
+    const lit::LitmusResult r = lit::run_litmus(spec, seed_begin, seed_end);
+    out->seeds_run = r.seeds_run;
+    out->assert_violations = r.assert_violations;
+    out->faults = r.faults;
+    out->distinct_outcomes = r.histogram.size();
+    if (histogram && histogram_cap > 0) {
+      std::vector<std::pair<uint64_t, std::string>> rows;
+      for (const auto& [o, c] : r.histogram) rows.emplace_back(c, o.to_string());
+      std::stable_sort(rows.begin(), rows.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      std::string text;
+      for (const auto& [c, o] : rows) text += std::to_string(c) + "\t" + o + "\n";
+      const size_t n = std::min<size_t>(text.size(), size_t(histogram_cap - 1));
+      std::memcpy(histogram, text.data(), n);
+      histogram[n] = 0;
+    }
+    if (r.faults) {
+      set_error("litmus: " + r.first_fault.detail);
+      return FORGE_ERR_DEVICE_FAULT;
+    }
     return FORGE_OK;
   });
 }

@@ -360,3 +360,28 @@ def device_count() -> int:
     c = C.c_int()
     _lib().forge_device_count(C.byref(c))
     return c.value
+
+
+# ---- litmus (forge::lit: reference proj/include/forge/litmus.hpp) -------------
+
+def parse_litmus(text: str) -> None:
+    """Validates a litmus program (reference parse_litmus, litmus.cpp:169-253);
+    raises ForgeError("ParseError") with the offending line."""
+    check(_lib().forge_litmus_parse(text.encode()))
+
+
+def run_litmus(text: str, seed_begin: int, seed_end: int) -> dict:
+    """Runs instances seed_begin .. seed_end-1 of the program on the GPU
+    (reference run_litmus, litmus.cpp:283-350; here each block is a CTA on
+    its own SM).  Returns seeds_run, assert_violations, faults and the
+    histogram {outcome string: count}."""
+    res = capi.LitmusResult()
+    buf = C.create_string_buffer(1 << 16)
+    check(_lib().forge_litmus_run(text.encode(), seed_begin, seed_end, C.byref(res), buf, len(buf)))
+    hist = {}
+    for line in buf.value.decode().splitlines():
+        count, outcome = line.split("\t", 1)
+        hist[outcome] = int(count)
+    return {"seeds_run": res.seeds_run, "assert_violations": res.assert_violations, "faults": res.faults,
+            "distinct_outcomes": res.distinct_outcomes, "histogram": hist}
+
