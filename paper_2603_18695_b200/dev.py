@@ -66,6 +66,8 @@ class Workspace:
     def __init__(self, device=None):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.buf = torch.zeros(256, dtype=torch.uint8, device=self.device)
+        self._shapes: dict = {}  # (prim, op, n, p_cols) -> (ptr, bytes, buffer generation)
+        self._gen = 0
 
     def ensure(self, nbytes: int, stream=None) -> torch.Tensor:
         """Grows the buffer to >= nbytes.  The new buffer is allocated and zeroed
@@ -80,11 +82,21 @@ class Workspace:
             with torch.cuda.stream(s):
                 self.buf = torch.zeros(max(nbytes, 2 * old.numel()), dtype=torch.uint8, device=self.device)
             old.record_stream(s)
+            self._gen += 1
         return self.buf
 
     def for_(self, prim: int, op: int, n: int, p_cols: int = 0, stream=None) -> tuple[int, int]:
+        # (ptr, bytes) per shape while the buffer stays the same: small launches
+        # are host-bound, and this is one dict lookup instead of four calls
+        key = (prim, op, n, p_cols)
+        hit = self._shapes.get(key)
+        if hit is not None and hit[2] == self._gen:
+            return hit[0], hit[1]
         need = workspace_bytes(prim, op, n, p_cols)
         b = self.buf if self.buf.numel() >= need else self.ensure(need, stream)
+        if len(self._shapes) > 64:
+            self._shapes.clear()
+        self._shapes[key] = (b.data_ptr(), b.numel(), self._gen)
         return b.data_ptr(), b.numel()
 
 
@@ -101,7 +113,9 @@ def fill_synthetic(op: int, dst: torch.Tensor, n: int, seed: int, index_base: in
 
 def mapreduce(op: int, src, n: int, out, ws: Workspace, stream=None) -> None:
     w, wb = ws.for_(capi.PRIM_MAPREDUCE, op, n, stream=stream)
-    check(_lib().forge_dev_mapreduce(op, _ptr(src), n, _ptr(out), w, wb, _stream(stream)))
+    rc = _lib().forge_dev_mapreduce(op, _ptr(src), n, _ptr(out), w, wb, _stream(stream))
+    if rc:
+        check(rc)
 
 
 def reduce_ordered(op: int, src, n: int, out, ws: Workspace, stream=None) -> None:
@@ -112,8 +126,10 @@ def reduce_ordered(op: int, src, n: int, out, ws: Workspace, stream=None) -> Non
 def scan(op: int, inclusive: bool, src, dst, n: int, ws: Workspace, carry_in=None, total_out=None,
          stream=None) -> None:
     w, wb = ws.for_(capi.PRIM_SCAN, op, n, stream=stream)
-    check(_lib().forge_dev_scan(op, 1 if inclusive else 0, _ptr(src), _ptr(dst), n, _ptr(carry_in),
-                                _ptr(total_out), w, wb, _stream(stream)))
+    rc = _lib().forge_dev_scan(op, 1 if inclusive else 0, _ptr(src), _ptr(dst), n, _ptr(carry_in),
+                               _ptr(total_out), w, wb, _stream(stream))
+    if rc:
+        check(rc)
 
 
 def matvec(op: int, A, n: int, p_cols: int, x, y, ws: Workspace, stream=None, lda: int = 0) -> None:
