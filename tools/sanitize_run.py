@@ -49,6 +49,9 @@ for op in (capi.MV_F32_PLUS_TIMES, capi.MV_F32_MIN_PLUS):
         yv = dev.empty(op, max(n, p), "S")
         dev.matvec(op, A, n, p, xv, yv, ws)
         dev.vecmat(op, A, n, p, xv, yv, ws)
+from paper_2603_18695_b200 import forge as F  # noqa: E402
+r = F.run_litmus("blocks=2 cells=2\nB0: st 0 =1\nB0: st 1 rel =1\nB1: ld 1 acq\nB1: ld 0\n", 0, 256)
+assert r["faults"] == 0
 a = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
 b = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
 a.fill_(7)
