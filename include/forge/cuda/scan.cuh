@@ -734,12 +734,9 @@ struct LagArgs {
   ScanArgs<T, S, F, Op> s;  // src, dst, f, op, identity, carry_in, total_out, ctrl, ntiles (full tiles)
   uint64_t* tagg;           // tile aggregates: STRIDE words per tile, compact
   uint64_t* gstate;         // group states: STRIDE words per group, compact
-  uint32_t dev_flags;       // FORGE_DEV probes (kLagDevSpecSmem)
   uint32_t lag;             // D
   uint32_t nclaims;         // ntiles + D
 };
-
-constexpr uint32_t kLagDevSpecSmem = 8;  // FORGE_DEV probe: speculative shared-memory load of blockIdx.x
 
 template <class T, class S, class F, class Op, bool Inclusive>
 __global__ void __launch_bounds__(kScanThreads, 6)
@@ -757,7 +754,7 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   const auto& a = L.s;
   extern __shared__ unsigned char dyn_smem[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t s_k, s_epoch, s_phase;
+  __shared__ uint32_t s_k, s_epoch;
   __shared__ Opt<A> s_warp[NW];
   __shared__ Opt<C> s_carry;
   __shared__ C s_carry_agg;  // A's tile aggregate
@@ -775,25 +772,15 @@ __global__ void __launch_bounds__(kScanThreads, 6)
   // ticket other than blockIdx.x, tools/trace_lag.py), but the tile a CTA
   // claims was prefetched by the CTA with that index, which started at about
   // the same time, so its shared-memory load right after the claim is an L2
-  // hit (or joins the fill in flight).  (A speculative shared-memory load of
+  // hit (or joins the fill in flight).  A speculative shared-memory load of
   // blockIdx.x instead had to land before the buffer could take the claimed
-  // tile: FORGE_DEV flag kLagDevSpecSmem.)
-  const bool spec_smem = (L.dev_flags & kLagDevSpecSmem) != 0;
+  // tile (affine 5.24 -> 5.62 TB/s with the prefetch).
   if (threadIdx.x == 0) {
     const uint32_t g = blockIdx.x;
     mbar_init(&bar, 1);
     fence_mbar_init();
     const uint64_t pol = l2_policy_evict_last();
-    if (g < a.ntiles) {
-      if (spec_smem) {
-        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
-        tma_load_2d_hint(buf, &tmap, 0, int(g) * kScanThreads, &bar, pol);
-      } else if (!a.prefetch_ahead || g < a.prefetch_ahead) {
-        tma_prefetch_2d_hint(&tmap, 0, int(g) * kScanThreads, pol);
-      }
-    }
-    if (!spec_smem && a.prefetch_ahead && uint64_t(g) + a.prefetch_ahead < a.ntiles)
-      tma_prefetch_2d_hint(&tmap, 0, int(g + a.prefetch_ahead) * kScanThreads, pol);
+    if (g < a.ntiles) tma_prefetch_2d_hint(&tmap, 0, int(g) * kScanThreads, pol);
     uint64_t* word = reinterpret_cast<uint64_t*>(a.ctrl);
     // relaxed: nothing is ordered by the claim (every tile state carries its
     // launch's epoch; the workspace memset precedes the launch).  An acq_rel
@@ -806,25 +793,17 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     if (k == L.nclaims - 1) st_relaxed_gpu(word, uint64_t(e + 1u) << 32);
     s_k = k;
     s_epoch = e;
-    uint32_t ph = 0;  // parity of the barrier's next completion
-    if (!spec_smem || k != g) {
-      if (spec_smem && g < a.ntiles) {
-        mbar_wait(&bar, 0);  // drain the speculative copy
-        ph = 1;
-      }
-      if (k < a.ntiles) {
-        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
-        tma_load_2d_hint(buf, &tmap, 0, int(k) * kScanThreads, &bar, pol);
-      }
+    if (k < a.ntiles) {
+      mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+      tma_load_2d_hint(buf, &tmap, 0, int(k) * kScanThreads, &bar, pol);
     }
-    s_phase = ph;
   }
   __syncthreads();
   const uint32_t k = s_k, epoch = s_epoch;
-  uint32_t phase = s_phase;
+  uint32_t phase = 0;  // parity of the barrier's next completion
   if (tr && threadIdx.x == 0) {
     tr[uint64_t(k) * 8 + 0] = t_start;
-    tr[uint64_t(k) * 8 + 1] = (global_ns() & ~uint64_t(1)) | uint64_t(k != blockIdx.x);  // LSB: speculative load missed
+    tr[uint64_t(k) * 8 + 1] = (global_ns() & ~uint64_t(1)) | uint64_t(k != blockIdx.x);  // LSB: ticket != blockIdx.x
   }
   const bool hasA = k < a.ntiles;
   const bool hasB = k >= L.lag && k - L.lag < a.ntiles;
@@ -1213,11 +1192,6 @@ inline uint32_t scan_lag() {
   static const uint32_t v = dev_knob("FORGE_SCAN_LAG", device_props().sm_count * 4);
   return v;
 }
-// FORGE_DEV knob FORGE_SCAN_LAG_FLAGS (kLagDevSpecSmem)
-inline uint32_t scan_lag_dev_flags() {
-  static const uint32_t v = dev_knob("FORGE_SCAN_LAG_FLAGS", 0);
-  return v;
-}
 // L2 prefetch distance of the single-pass tile kernel, in tiles: CTA g
 // prefetches tile g + ahead, so the tile a CTA claims is in L2 before the
 // claim returns.  Measured (2^28, GB/s, f32 / i32 / argmax): ahead 0 (the
@@ -1345,7 +1319,6 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
         LagArgs<T, S, F, Op> L{a,
                                reinterpret_cast<uint64_t*>(w + LW::tagg_off(nfull)),
                                reinterpret_cast<uint64_t*>(w + LW::gstate_off(nfull)),
-                               scan_lag_dev_flags(),
                                lag,
                                uint32_t(nfull + lag)};
         L.s.ntiles = uint32_t(nfull);

@@ -48,11 +48,11 @@ life = (end - raw[:, 0]) / 1e3
 d["lifetime_all_mean_us"] = round(float(life.mean()), 3)
 mid = (end.max() + t0) / 2
 d["alive_at_mid"] = int(((raw[:, 0] <= mid) & (end >= mid)).sum())
-d["spec_load_miss_frac"] = round(float((raw[:, 1] & 1).mean()), 4)  # ticket != blockIdx.x
+d["ticket_ne_blockidx_frac"] = round(float((raw[:, 1] & 1).mean()), 4)
 miss = (raw[:, 1] & 1) == 1
 if miss.any() and (~miss).any():
     la = (raw[:, 2] - raw[:, 0]) / 1e3
     ok2 = raw[:, 2] > 0
-    d["start->A_landed_hit_us"] = round(float(la[ok2 & ~miss].mean()), 3)
-    d["start->A_landed_miss_us"] = round(float(la[ok2 & miss].mean()), 3)
+    d["start->A_landed_ticket_eq_blockidx_us"] = round(float(la[ok2 & ~miss].mean()), 3)
+    d["start->A_landed_ticket_ne_blockidx_us"] = round(float(la[ok2 & miss].mean()), 3)
 print(json.dumps(d))
