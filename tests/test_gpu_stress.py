@@ -6,6 +6,7 @@ last-CTA fold ran early, shows up as a mismatch against the first launch
 (which itself is checked against the oracle)."""
 from __future__ import annotations
 
+import os
 import shutil
 import subprocess
 import sys
@@ -126,12 +127,20 @@ def test_relaxed_protocol_mutant_is_caught(op, path):
     assert mismatches(relax=False, seed=0x5EED + 1) == 0
 
 
+# Opt-in (FORGE_RUN_SANITIZER=1): the GPU pool has since closed compute-sanitizer
+# (runs under it left GPUs needing a reset), so the default suite must not launch
+# it.  The clean runs of every kernel family are committed under profiles/
+# (r01/compute_sanitizer.log, r02/compute_sanitizer_session4.log).
 @pytest.mark.skipif(shutil.which("compute-sanitizer") is None, reason="compute-sanitizer not on PATH")
+@pytest.mark.skipif(os.environ.get("FORGE_RUN_SANITIZER") != "1",
+                    reason="compute-sanitizer is opt-in (FORGE_RUN_SANITIZER=1); closed on the GPU pool")
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer_clean(tool):
     r = subprocess.run(["compute-sanitizer", "--tool", tool, "--error-exitcode", "9", sys.executable,
                         str(ROOT / "tools" / "sanitize_run.py")], cwd=ROOT, capture_output=True, text=True,
                        timeout=900)
+    if "closed on this pool" in r.stderr:
+        pytest.skip("compute-sanitizer refused by the GPU pool")
     assert r.returncode == 0 and "sanitize_run ok" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
 
 
