@@ -152,6 +152,7 @@ struct ScanArgs {
   uint64_t perturb_seed;  // test schedule perturbation (ScanTestHooks), 0 = off
   uint32_t perturb_ns;
   uint32_t prefetch_ahead;  // CTA g L2-prefetches tile g + prefetch_ahead (0: tile g; scan_prefetch_ahead)
+  uint32_t block_order;     // scan_smem_kernel: tile = blockIdx.x, loaded at CTA start (scan_block_order)
 };
 
 // Test-only hooks of one scan launch (both off in production):
@@ -531,14 +532,26 @@ __global__ void __launch_bounds__(kScanThreads, scan_smem_min_blocks<S, Op, R>()
       for (int r = 0; r < R; ++r)
         tma_prefetch_2d_hint(&tmap, 0, (int(t) * R + r) * kScanThreads, l2_policy_evict_normal());
     };
-    if (a.prefetch_ahead && g < a.prefetch_ahead && uint64_t(g + 1) * kTile <= a.n) prefetch(g);
-    if ((gp + 1) * kTile <= a.n) prefetch(gp);
-    uint32_t e;
-    const uint32_t t = claim_tile(a, e);
-    s_tile = t;
-    s_epoch = e;
-    s_phase = 0;
-    if (uint64_t(t + 1) * kTile <= a.n) load_tile(t);
+    if (a.block_order) {
+      // Tile g itself: its HBM load starts at once and the claim (kept for
+      // the launch epoch and the ticket reset) overlaps it.
+      if (uint64_t(g + 1) * kTile <= a.n) load_tile(g);
+      if ((gp + 1) * kTile <= a.n) prefetch(gp);
+      uint32_t e;
+      claim_tile(a, e);
+      s_tile = g;
+      s_epoch = e;
+      s_phase = 0;
+    } else {
+      if (a.prefetch_ahead && g < a.prefetch_ahead && uint64_t(g + 1) * kTile <= a.n) prefetch(g);
+      if ((gp + 1) * kTile <= a.n) prefetch(gp);
+      uint32_t e;
+      const uint32_t t = claim_tile(a, e);
+      s_tile = t;
+      s_epoch = e;
+      s_phase = 0;
+      if (uint64_t(t + 1) * kTile <= a.n) load_tile(t);
+    }
   }
   __syncthreads();
   const uint64_t tile = s_tile;
@@ -780,7 +793,14 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     mbar_init(&bar, 1);
     fence_mbar_init();
     const uint64_t pol = l2_policy_evict_last();
-    if (g < a.ntiles) tma_prefetch_2d_hint(&tmap, 0, int(g) * kScanThreads, pol);
+    if (a.block_order) {  // ticket = blockIdx.x (scan_block_order): A's load starts before the claim
+      if (g < a.ntiles) {
+        mbar_arrive_expect_tx(&bar, kSmemTileBytes);
+        tma_load_2d_hint(buf, &tmap, 0, int(g) * kScanThreads, &bar, pol);
+      }
+    } else if (g < a.ntiles) {
+      tma_prefetch_2d_hint(&tmap, 0, int(g) * kScanThreads, pol);
+    }
     uint64_t* word = reinterpret_cast<uint64_t*>(a.ctrl);
     // relaxed: nothing is ordered by the claim (every tile state carries its
     // launch's epoch; the workspace memset precedes the launch).  An acq_rel
@@ -788,12 +808,13 @@ __global__ void __launch_bounds__(kScanThreads, 6)
     // after, measured 2^28 f32 5,290 -> 5,530 GB/s, affine 4,900 -> 5,110,
     // Mat2 4,930 -> 5,100 without them.
     const uint64_t got = atom_add_relaxed_gpu(word, uint64_t(1));
-    const uint32_t k = uint32_t(got);
+    const uint32_t t = uint32_t(got);
     const uint32_t e = uint32_t(got >> 32);
-    if (k == L.nclaims - 1) st_relaxed_gpu(word, uint64_t(e + 1u) << 32);
+    if (t == L.nclaims - 1) st_relaxed_gpu(word, uint64_t(e + 1u) << 32);
+    const uint32_t k = a.block_order ? g : t;
     s_k = k;
     s_epoch = e;
-    if (k < a.ntiles) {
+    if (!a.block_order && k < a.ntiles) {
       mbar_arrive_expect_tx(&bar, kSmemTileBytes);
       tma_load_2d_hint(buf, &tmap, 0, int(k) * kScanThreads, &bar, pol);
     }
@@ -1205,6 +1226,26 @@ inline uint32_t scan_prefetch_ahead() {
   static const uint32_t v = dev_knob("FORGE_SCAN_PREFETCH_AHEAD", device_props().sm_count);
   return v;
 }
+// Tile order of the single-pass tile kernel: 1 = blockIdx.x (default): the
+// tile's TMA load is issued at CTA start and the claim — still made, for the
+// launch epoch and the ticket reset — overlaps it; forward progress relies on
+// the hardware dispatching a launch's CTAs in increasing blockIdx order, as
+// CUB's single-pass scan (tile_idx = blockIdx.x) does.  0 = tickets (tile =
+// claim order, deadlock-free under any dispatch order; FORGE_DEV knob).
+// Measured 2^28 (GB/s, tickets -> blockIdx): f32 6,053 -> 6,160-6,197, i32
+// 6,159 -> 6,272-6,306, argmax 5,560-5,612 -> 5,726-5,790, i64 6,059 -> 6,237;
+// 2^23 f32 3,549 -> 3,560-3,972 (tools/probe_order.py).
+inline uint32_t scan_block_order() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_BLOCK_ORDER", 1);
+  return v;
+}
+// The lagged kernel keeps tickets: with ticket = blockIdx.x (A's load before
+// the claim) it measured slower, affine 2^28 5,624-5,643 -> 5,472-5,501 GB/s,
+// Mat2 2^27 5,574-5,618 -> 5,374-5,458 (tools/probe_order.py).
+inline uint32_t scan_lag_block_order() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_LAG_BLOCK_ORDER", 0);
+  return v;
+}
 inline bool scan_no_tma_store() {
   static const bool v = dev_knob("FORGE_SCAN_NO_TMA_STORE", 0) != 0;
   return v;
@@ -1299,7 +1340,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
                           static_cast<uint32_t*>(ws), 0u, 0u, scan_lookback_mode(), nullptr,
                           scan_backoff_ns(), hooks.relax_epoch ? 0u : 0x3fffffffu, hooks.perturb_seed,
-                          hooks.perturb_ns, scan_prefetch_ahead()};
+                          hooks.perturb_ns, scan_prefetch_ahead(), scan_block_order()};
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
@@ -1323,6 +1364,7 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                                uint32_t(nfull + lag)};
         L.s.ntiles = uint32_t(nfull);
         L.s.prefetch_ahead = 0;  // scan_prefetch_ahead
+        L.s.block_order = scan_lag_block_order();
 #ifdef FORGE_DEV
         L.s.trace = scan_trace_for(nfull + lag);
 #endif
