@@ -4,9 +4,11 @@
 // aggregate published as PARTIAL, look-back over predecessors until a PREFIX,
 // own PREFIX published, outputs composed and stored once), re-designed for the
 // hardware:
-//   * tile ids come from an atomic ticket, not blockIdx.x (the VM admitted
-//     blocks in id order, machine.cpp:767-776; CUDA guarantees no such order,
-//     so a tile could otherwise spin on a predecessor that never runs);
+//   * tile ids: the TMA tile kernel uses blockIdx.x (its load starts at CTA
+//     start; forward progress rests on in-order CTA dispatch, as in CUB's
+//     single-pass scan — the VM admitted blocks in id order too,
+//     machine.cpp:767-776); the lagged and register kernels take an atomic
+//     ticket (deadlock-free under any dispatch order; scan_block_order);
 //   * tile status: every 32-bit chunk of the published value travels in its
 //     own 64-bit word {status, chunk}; a reader accepts a state only when all
 //     words carry the same status — no fence, no separate flag byte (the
@@ -15,10 +17,11 @@
 //     granularity and every CTA in flight polls the newest tiles' states, so
 //     packed 8-16-byte states put the hottest lines on ONE slice (measured
 //     +25% scan bandwidth, profiles/);
-//   * status = (epoch << 2) | {1 PARTIAL, 2 PREFIX}: every CTA reads the epoch
-//     before its acq_rel ticket claim, and the LAST claimer advances it for the
-//     next launch, so stale states of earlier launches read as INVALID and the
-//     workspace needs no fill_zero per launch (primitives.hpp:464-466);
+//   * status = (epoch << 2) | {1 PARTIAL, 2 PREFIX}: every CTA gets the epoch
+//     from its relaxed 64-bit {epoch, ticket} claim, and the LAST claimer
+//     advances it for the next launch, so stale states of earlier launches
+//     read as INVALID and the workspace needs no fill_zero per launch
+//     (primitives.hpp:464-466);
 //   * look-back: warp 0 polls 32 predecessors per L2 round trip, finds the
 //     nearest PREFIX with one ballot and folds the window with a log-step
 //     ORDER-PRESERVING reduction (the reference folded it serially,
