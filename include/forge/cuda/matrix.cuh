@@ -264,12 +264,10 @@ constexpr int gemv_vec_elems() {
   return mr_vec_elems<T>();
 }
 
-// U: columns whose loads are issued together per thread; MinB: resident CTAs
-// per SM the registers are budgeted for; Pipe: the next U columns are loaded
-// before the current U are folded (2U loads in flight per thread).
-template <class T, class S, class F2, class Op, bool UsesX, int U = 4, int MinB = 1, bool Pipe = false>
-__global__ void __launch_bounds__(kMatThreads, MinB) gemv_kernel(const GemvArgs<T, S, F2, Op> a) {
+template <class T, class S, class F2, class Op, bool UsesX>
+__global__ void __launch_bounds__(kMatThreads) gemv_kernel(const GemvArgs<T, S, F2, Op> a) {
   constexpr int VE = gemv_vec_elems<T>();
+  constexpr int U = 4;
   __shared__ bool s_last;
   const uint32_t rb = blockIdx.x % a.row_blocks;
   const uint32_t s = blockIdx.x / a.row_blocks;
@@ -291,42 +289,6 @@ __global__ void __launch_bounds__(kMatThreads, MinB) gemv_kernel(const GemvArgs<
 #pragma unroll
         for (int e = 0; e < VE; ++e) acc[e] = fa(av[e], xj);
         ++j;
-      }
-      if constexpr (Pipe) {
-        if (j + U <= c1) {
-          T cur[U][VE];
-          T xc[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            load_items<T, VE>(a.A + (j + u) * a.lda + i0, cur[u]);
-            xc[u] = UsesX ? a.x[j + u] : xz;
-          }
-          j += U;
-#pragma unroll 2
-          for (; j + U <= c1; j += U) {
-            T nxt[U][VE];
-            T xn[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              load_items<T, VE>(a.A + (j + u) * a.lda + i0, nxt[u]);
-              xn[u] = UsesX ? a.x[j + u] : xz;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-              for (int e = 0; e < VE; ++e) acc[e] = a.op(acc[e], fa(cur[u][e], xc[u]));
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              xc[u] = xn[u];
-#pragma unroll
-              for (int e = 0; e < VE; ++e) cur[u][e] = nxt[u][e];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int e = 0; e < VE; ++e) acc[e] = a.op(acc[e], fa(cur[u][e], xc[u]));
-        }
       }
       for (; j + U <= c1; j += U) {
         T av[U][VE];
