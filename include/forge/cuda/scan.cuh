@@ -1155,7 +1155,13 @@ struct ScanWs {
 };
 
 #ifndef FORGE_SCAN_LAG_MAX_T
-#define FORGE_SCAN_LAG_MAX_T 16  // largest element (bytes) taken by the lagged scan
+// largest element (bytes) taken by the lagged scan.  16-byte elements (Mat2)
+// take the single-pass kernel since its tiles are blockIdx-ordered: Mat2 2^27
+// 5,759-5,823 GB/s single-pass vs 5,574-5,618 lagged (tools/probe_order.py,
+// profiles/r02/probe_order_single_pass_all_session5.log); 8-byte elements with
+// 16-byte carries (f32 affine, f64 carry) keep the lagged kernel (5,624-5,643
+// vs 5,605).
+#define FORGE_SCAN_LAG_MAX_T 8
 #endif
 
 // Lagged-scan workspace: [256-byte control block | tile

@@ -1,15 +1,17 @@
 """The lagged scan (include/forge/cuda/scan.cuh scan_lag_kernel, the default
 for contiguous scans of >= 3 lags of full tiles (3 x 4 tiles per SM) with
-sizeof(T) = sizeof(S) <= 16 and 16-byte carries: affine, Mat2) at its
-boundaries, against the CPU oracle; the 4- and 8-byte-carry ops in the same
-tests take the single-pass kernel at the same sizes:
+sizeof(T) = sizeof(S) <= 8 and 16-byte carries: f32 affine with its f64
+carry) at its boundaries, against the CPU oracle; the other ops in the same
+tests (4- and 8-byte carries, 16-byte Mat2 elements) take the single-pass
+kernel at the same sizes:
 
 * the full-tile threshold (one below / at / above) and larger counts, plus
   sizes below it (the single-pass kernel);
 * a partial last tile (the tail launch seeded with the full tiles' total);
 * carry_in and total_out through the device-pointer layer (the sharded
   scan's carry), inclusive and exclusive;
-* 16-byte elements (Mat2, lagged) next to quaternions (single-pass);
+* 16-byte elements (Mat2, single-pass since blockIdx tile order) next to
+  quaternions (single-pass, 32-byte carry);
 * one workspace reused across sizes whose layouts overlap (the tail's
   sub-workspace moves with the full-tile count).
 """

@@ -68,7 +68,7 @@ def test_mapreduce_relaunch_stress():
 
 
 @pytest.mark.parametrize("path", ["single_pass", "lagged"])
-@pytest.mark.parametrize("op", [capi.I32_SUM, capi.MAT2_U32, capi.F32_SUM])
+@pytest.mark.parametrize("op", [capi.I32_SUM, capi.MAT2_U32, capi.F32_SUM, capi.AFFINE_F32])
 def test_relaxed_protocol_mutant_is_caught(op, path):
     # The ordering ablation (MutationFlags::relax_scan_flag,
     # reference primitives.hpp:64-67): with the epoch tag of the tile states
@@ -82,9 +82,10 @@ def test_relaxed_protocol_mutant_is_caught(op, path):
     # checked bit for bit.  The product protocol must pass under the same
     # schedule, the mutant must be caught.
     # path "lagged": above the lagged scan's threshold (3 lags of 4 tiles per
-    # SM, include/forge/cuda/scan.cuh), where Mat2 (16-byte carry) takes the
-    # lagged kernel, whose A phases publish the aggregates the mutant may
-    # confuse with the previous launch's (i32 / f32: the single-pass kernel)
+    # SM, include/forge/cuda/scan.cuh), where affine (8-byte elements, 16-byte
+    # f64 carry) takes the lagged kernel, whose A phases publish the aggregates
+    # the mutant may confuse with the previous launch's (i32 / f32 / Mat2: the
+    # single-pass kernel, blockIdx-ordered tiles)
     lib = capi.load()
     if path == "single_pass":
         n = (1 << 22) + 17

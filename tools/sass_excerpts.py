@@ -20,7 +20,7 @@ funcs = re.split(r"\n\s+Function : ", sass)
 # family -> substring of the mangled name that picks one representative
 FAMILIES = {
     "scan_lag_kernel (affine, f64 carry)": ("scan_lag_kernel", "AffineOpELb1"),
-    "scan_lag_kernel (Mat2, 16-byte carry)": ("scan_lag_kernel", "Mat2MulELb1"),
+    "scan_smem_kernel (Mat2, 16-byte elements, R = 2)": ("scan_smem_kernel", "Mat2MulELb1ELi2"),
     "scan_smem_kernel (f32 sum, TMA tile)": ("scan_smem_kernel", "IffNS_3alg8IdentityENS_4menu6AddF32ELb1"),
     "scan_smem_kernel (affine, f64 carry)": ("scan_smem_kernel", "AffineOpELb1"),
     "scan_smem_kernel (argmax)": ("scan_smem_kernel", "ArgMaxOpELb1"),
