@@ -1255,6 +1255,16 @@ inline uint32_t scan_lag_block_order() {
   static const uint32_t v = dev_knob("FORGE_SCAN_LAG_BLOCK_ORDER", 0);
   return v;
 }
+// Prefetch distance of the blockIdx-ordered single-pass kernel (its own tile
+// is TMA-loaded at CTA start; the prefetch serves the CTAs of later waves):
+// measured 2^28 (GB/s) at 0 / 1 / 2 / 3 tiles per SM: f32 5,695 / 6,199-6,201
+// / 6,237 / 6,236, i32 5,633 / 6,310-6,313 / 6,383 / 6,382, i64 5,757 /
+// 6,240-6,258 / 6,299 / 6,314, argmax 5,249 / 5,742 / 5,743 / 5,743, Mat2
+// (64 KB tiles) 5,308 / 5,759-5,774 / 5,774 / 5,307 — two tiles per SM.
+inline uint32_t scan_block_prefetch_ahead() {
+  static const uint32_t v = dev_knob("FORGE_SCAN_BLOCK_PREFETCH_AHEAD", 2 * device_props().sm_count);
+  return v;
+}
 inline bool scan_no_tma_store() {
   static const bool v = dev_knob("FORGE_SCAN_NO_TMA_STORE", 0) != 0;
   return v;
@@ -1349,7 +1359,9 @@ cudaError_t launch_scan(const T* src, uint64_t src_stride, S* dst, uint64_t dst_
                           reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256),
                           static_cast<uint32_t*>(ws), 0u, 0u, scan_lookback_mode(), nullptr,
                           scan_backoff_ns(), hooks.relax_epoch ? 0u : 0x3fffffffu, hooks.perturb_seed,
-                          hooks.perturb_ns, scan_prefetch_ahead(), scan_block_order()};
+                          hooks.perturb_ns,
+                          scan_block_order() ? scan_block_prefetch_ahead() : scan_prefetch_ahead(),
+                          scan_block_order()};
   // The TMA tile kernel is instantiated only for power-of-two element sizes
   // up to 16 bytes (whole items per 16-byte chunk); other types take the
   // register kernel.
