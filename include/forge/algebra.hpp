@@ -184,11 +184,14 @@ struct ArgMax {
 // arg-max of data containing NaN is its first NaN); -0 == +0 ties by index.
 // A total preorder on v, so the op is associative and commutative for every
 // input, NaN included.  (Branch-free selects: as cheap as the NaN-unaware form.)
+// sa / sb: a / b strictly better.  !(x <= y) is "x > y or unordered" (one
+// FSETP.GTU): with the other side's NaN masked off it is exactly "x > y, or x
+// NaN and y not" — 4 FSETP per combine instead of 5.
 FORGE_HD ArgMax argmax_combine(const ArgMax& a, const ArgMax& b) {
   const bool an = is_nan_f32(a.v), bn = is_nan_f32(b.v);
-  const bool ta = (a.v > b.v) | (an & !bn);
-  const bool tb = (b.v > a.v) | (bn & !an);
-  return (ta | (!tb & (a.i <= b.i))) ? a : b;
+  const bool sa = !(a.v <= b.v) & !bn;
+  const bool sb = !(b.v <= a.v) & !an;
+  return (sa | (!sb & (a.i <= b.i))) ? a : b;
 }
 
 // ---- operator helpers (algebra.hpp:85-100)
