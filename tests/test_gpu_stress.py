@@ -178,3 +178,51 @@ def test_lagged_scan_relaunch_watchdog(op):
             assert torch.equal(y, first), (op, i)
     if op != capi.AFFINE_F32:
         assert torch.equal(y, first)
+
+
+def test_blockidx_ordered_scans_on_concurrent_streams():
+    # The single-pass tile kernel takes tile = blockIdx.x, so its forward
+    # progress rests on each launch's CTAs being dispatched in index order
+    # (scan.cuh scan_block_order).  Launches on different streams interleave
+    # their CTAs on the SMs; each must still finish.  Three scans (f32, argmax,
+    # Mat2 — the R = 1 and R = 2 tile shapes) run concurrently on three streams
+    # with their own workspaces, 40 rounds under a host watchdog; every output
+    # equals its stream's first (oracle-checked) result.
+    import time
+    ops = [capi.F32_SUM, capi.ARGMAX_F32I32, capi.MAT2_U32]
+    streams = [torch.cuda.Stream() for _ in ops]
+    wss = [dev.Workspace() for _ in ops]
+    xs, ys, firsts, ns = [], [], [], []
+    for k, op in enumerate(ops):
+        n = ((1 << 25) if F.op_info(op)["t_size"] <= 8 else (1 << 24)) + 4099 * (k + 1)
+        x = dev.empty(op, n)
+        dev.fill_synthetic(op, x, n, 0xC0C0 + k)
+        y = dev.empty(op, n, "S")
+        dev.scan(op, True, x, y, n, wss[k])
+        torch.cuda.synchronize()
+        got = y.cpu().numpy().view(np.uint8).view(F.s_dtype(op))
+        assert orc.check_scan_synthetic(op, True, n, 0xC0C0 + k, got, 1e-5)[0] == 0
+        xs.append(x)
+        ys.append(y)
+        firsts.append(y.clone())
+        ns.append(n)
+    for s in streams:
+        s.wait_stream(torch.cuda.current_stream())
+    for rnd in range(40):
+        evs = []
+        for k, op in enumerate(ops):
+            with torch.cuda.stream(streams[k]):
+                dev.scan(op, True, xs[k], ys[k], ns[k], wss[k], stream=streams[k])
+                ev = torch.cuda.Event()
+                ev.record(streams[k])
+                evs.append(ev)
+        t0 = time.time()
+        while not all(e.query() for e in evs):
+            if time.time() - t0 > 10:
+                sys.stderr.write(f"concurrent scans hung in round {rnd}\n")
+                sys.stderr.flush()
+                os._exit(3)
+            time.sleep(0.0002)
+    torch.cuda.synchronize()
+    for k, op in enumerate(ops):  # every kernel is deterministic (fixed fold order)
+        assert torch.equal(ys[k], firsts[k]), op
